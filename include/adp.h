@@ -1,0 +1,149 @@
+/*
+ * adp.h -- C-ABI drop-in boundary of the B200-native AdaPolySI Chebyshev-filter
+ * hot path (libadp_b200.so).
+ *
+ * The reference (arxiv 2604.00914, /root/reference/proj) has no FFI layer: its
+ * boundary is a set of C++ functions taking Eigen types. Each entry point below
+ * replaces one of them; the comment names the reference declaration (file:line
+ * relative to /root/reference/proj). Conventions:
+ *   - plain pointers and sizes only, no C++ or torch types, no exceptions;
+ *   - every call returns adp_status; the reference exception type maps 1:1 onto
+ *     ADP_ERR_CONFIG / ADP_ERR_DIMENSION / ADP_ERR_NOT_PD / ADP_ERR_PARSE
+ *     (include/adapoly/types.hpp:23-46); CUDA / NCCL / allocation failures get
+ *     their own codes; adp_last_error_message() returns the message of the
+ *     calling thread's last failure;
+ *   - host dense operands default to column-major (Eigen's default storage,
+ *     include/adapoly/types.hpp:13-20); device operands are row-major n x q with
+ *     a leading dimension (the B200 kernel layout);
+ *   - complex128 operands are interleaved (re, im) pairs (std::complex<double>);
+ *   - calls are ordered on the context's stream and synchronise before returning
+ *     host data. One host thread per context.
+ */
+#ifndef ADP_H_
+#define ADP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ADP_OK = 0,
+  ADP_ERR_CONFIG = 1,    /* adapoly::ConfigError        (types.hpp:40-42)   */
+  ADP_ERR_DIMENSION = 2, /* adapoly::DimensionError     (types.hpp:36-38)   */
+  ADP_ERR_NOT_PD = 3,    /* adapoly::NotPositiveDefinite (types.hpp:44-46)  */
+  ADP_ERR_PARSE = 4,     /* adapoly::ParseError         (types.hpp:23-34)   */
+  ADP_ERR_RUNTIME = 5,   /* std::runtime_error / std::invalid_argument      */
+  ADP_ERR_CUDA = 6,      /* CUDA runtime / cuBLAS / cuSOLVER failure        */
+  ADP_ERR_OOM = 7,       /* device allocation failed                        */
+  ADP_ERR_NCCL = 8       /* collective failure (multi-GPU row partition)    */
+} adp_status;
+
+typedef enum { ADP_F64 = 0, ADP_C128 = 1 } adp_dtype;
+typedef enum { ADP_COL_MAJOR = 0, ADP_ROW_MAJOR = 1 } adp_layout;
+typedef enum { ADP_DAMP_LANCZOS = 0, ADP_DAMP_JACKSON = 1 } adp_damping;
+
+typedef struct adp_ctx adp_ctx; /* device, stream, library handles, workspace */
+typedef struct adp_csr adp_csr; /* device-resident CSR operator               */
+
+/* ChebFilter minus its coefficient array (include/adapoly/cheb_filter.hpp:41-66). */
+typedef struct {
+  double interval_a, interval_b;
+  double alpha, beta;
+  int32_t k_max;
+  double m;
+  double l1, l2;
+  double lambda_min, lambda_max;
+  int32_t active_degree;
+} adp_filter_info;
+
+/* ---------------------------------------------------------------- context -- */
+int32_t adp_version(void);
+const char* adp_last_error_message(void);
+adp_status adp_ctx_create(int32_t device, adp_ctx** out);
+adp_status adp_ctx_destroy(adp_ctx* ctx);
+/* Run all subsequent work of ctx on an existing cudaStream_t (e.g. torch's). 0 = ctx's own stream. */
+adp_status adp_ctx_set_stream(adp_ctx* ctx, void* cuda_stream);
+adp_status adp_ctx_synchronize(adp_ctx* ctx);
+/* Number of kernels this library has launched on ctx (instrumentation for bench.py). */
+int64_t adp_ctx_launch_count(const adp_ctx* ctx);
+/* Kernel tuning knobs (0 = automatic): columns per warp task (panel width). */
+adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
+
+/* -------------------------------------------------------------- operator -- */
+/* Upload a CSR matrix (CsrMatrix, include/adapoly/csr_matrix.hpp:22-117: int64
+ * row_ptr / col_idx, columns strictly increasing within a row). Replaces
+ * csr_to_tiled (include/adapoly/tiled_matrix.hpp:58-94): the device keeps CSR
+ * with int32 column indices and int32 (nnz < 2^31) or int64 row offsets. Host
+ * arrays are copied; the caller keeps ownership. values: double[nnz] or
+ * interleaved complex128[nnz]. Columns must be sorted ascending per row: the
+ * kernel accumulates in CSR order, which is the reference's ascending-column
+ * order (tiled_matrix.hpp:78-81,200). */
+adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                          const int64_t* col_idx, const void* values, adp_dtype dtype, adp_csr** out);
+adp_status adp_csr_destroy(adp_csr* a);
+adp_status adp_csr_info(const adp_csr* a, int64_t* n_rows, int64_t* n_cols, int64_t* nnz, int32_t* dtype);
+
+/* clenshaw_apply (include/adapoly/cheb_filter.hpp:84-86, src/cheb_filter.cpp:129-179):
+ * Y = rho(l(A)) X with host X / Y. coeffs = ChebFilter::coeffs (k_max+1 doubles),
+ * l1 / l2 = ChebFilter::l1 / l2. Same semantics as the reference: degree in
+ * [0, k_max] else ADP_ERR_CONFIG; n_cols(A) != rows(X) -> ADP_ERR_DIMENSION;
+ * trailing zero coefficients reduce the degree; degrees 0 / 1 use the direct
+ * formulas; *spmv_count (if non-null) is incremented by effective_degree * q.
+ * Bitwise identical to the reference's arithmetic (no FMA contraction). */
+adp_status adp_filter_apply(adp_ctx* ctx, const adp_csr* a, const double* coeffs, int32_t k_max, double l1,
+                            double l2, int32_t degree, const void* x, int64_t x_rows, int64_t ldx, int64_t q,
+                            adp_layout layout, void* y, int64_t ldy, int64_t* spmv_count);
+/* Same on device-resident row-major operands (x: n x q with leading dimension
+ * ldx, y: n x q with ldy; y may alias nothing in x). Stream-ordered, no sync. */
+adp_status adp_filter_apply_device(adp_ctx* ctx, const adp_csr* a, const double* coeffs, int32_t k_max, double l1,
+                                   double l2, int32_t degree, const void* dx, int64_t x_rows, int64_t ldx, int64_t q,
+                                   void* dy, int64_t ldy, int64_t* spmv_count);
+
+/* maspmm (include/adapoly/tiled_matrix.hpp:184-186): C += A B (accumulate != 0)
+ * or C = A B (accumulate == 0; the reference's set_zero() + maspmm). Host
+ * operands in the given layout; k = columns of B. */
+adp_status adp_spmm(adp_ctx* ctx, const adp_csr* a, const void* b, int64_t b_rows, int64_t ldb, int64_t k,
+                    adp_layout layout, void* c, int64_t ldc, int32_t accumulate);
+adp_status adp_spmm_device(adp_ctx* ctx, const adp_csr* a, const void* db, int64_t b_rows, int64_t ldb, int64_t k,
+                           void* dc, int64_t ldc, int32_t accumulate);
+
+/* ---------------------------------------------- filter construction (host) -- */
+/* chebyshev_step_coeffs (src/cheb_filter.cpp:21-37); out: k+1 doubles. */
+adp_status adp_step_coeffs(double alpha, double beta, int32_t k, double* out);
+/* lanczos_damping (src/cheb_filter.cpp:39-49) / jackson_damping (:51-61). */
+adp_status adp_lanczos_damping(int32_t k, double m, double* out);
+adp_status adp_jackson_damping(int32_t k, double* out);
+/* build_filter (src/cheb_filter.cpp:63-94); coeffs: k+1 doubles. */
+adp_status adp_build_filter(double a, double b, double lambda_min, double lambda_max, int32_t k, double m,
+                            adp_damping damping, adp_filter_info* info, double* coeffs);
+/* eval_filter_scalar (src/cheb_filter.cpp:96-127); *clamped (nullable) += clamp count. */
+adp_status adp_eval_filter(const adp_filter_info* f, const double* coeffs, const double* x, int64_t n,
+                           int32_t degree, double* out, int64_t* clamped);
+/* initial_degree (src/cheb_filter.cpp:181-187). */
+adp_status adp_initial_degree(double alpha, double beta, double c, int32_t* out);
+/* adaptive_degree (src/cheb_filter.cpp:189-219). */
+adp_status adp_adaptive_degree(const adp_filter_info* f, const double* coeffs, const double* ritz, int64_t p,
+                               int64_t e_i, double tau_a, int32_t* out);
+
+/* ------------------------------------------------------------- seeded RNG -- */
+/* fill_gaussian / fill_rademacher (include/adapoly/philox.hpp:92-109) into a
+ * host column-major n x q buffer: Philox4x32-10, draw index c*n + r. */
+adp_status adp_fill_gaussian(double* out, int64_t n, int64_t q, uint64_t seed, uint64_t stream);
+adp_status adp_fill_rademacher(double* out, int64_t n, int64_t q, uint64_t seed, uint64_t stream);
+/* Philox4x32-10 primitives (philox.hpp:25-72): gaussian / uniform draws
+ * first..first+count-1 of (seed, stream), and one raw 4-word block. */
+adp_status adp_philox_gaussian(uint64_t seed, uint64_t stream, uint64_t first, int64_t count, double* out);
+adp_status adp_philox_uniform(uint64_t seed, uint64_t stream, uint64_t first, int64_t count, double* out);
+adp_status adp_philox_block(uint64_t seed, uint64_t stream, uint64_t counter, uint32_t* out);
+/* The same draws generated on the device into a row-major n x q block (ld). */
+adp_status adp_fill_gaussian_device(adp_ctx* ctx, double* d_out, int64_t n, int64_t q, int64_t ld, uint64_t seed,
+                                    uint64_t stream);
+adp_status adp_fill_rademacher_device(adp_ctx* ctx, double* d_out, int64_t n, int64_t q, int64_t ld,
+                                      uint64_t seed, uint64_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADP_H_ */

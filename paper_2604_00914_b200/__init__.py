@@ -1,0 +1,23 @@
+"""B200-native AdaPolySI Chebyshev-filter hot path (arxiv 2604.00914).
+
+Host-side mirror of the reference's operator / filter API over the C-ABI of
+libadp_b200.so (include/adp.h). The CUDA path is the only path: there is no
+CPU fallback, and calls raise if the shared library is not built.
+"""
+from ._native import (AdpError, CollectiveError, ConfigError, CudaError, DimensionError, NotPositiveDefinite,
+                      OutOfMemory, ParseError, lib)
+from .filter import (ChebFilter, SpectrumBounds, adaptive_degree, build_filter, chebyshev_step_coeffs,
+                     eval_filter_scalar, initial_degree, jackson_damping, lanczos_damping)
+from .operator import (Context, DeviceCsr, clenshaw_apply, clenshaw_apply_device, default_context, maspmm,
+                       maspmm_device)
+from .sparse import (CsrMatrix, fill_gaussian, fill_rademacher, parse_matrix_market, philox_block,
+                     philox_gaussian, philox_uniform, read_matrix_market)
+
+__all__ = [
+    "AdpError", "CollectiveError", "ConfigError", "CudaError", "DimensionError", "NotPositiveDefinite",
+    "OutOfMemory", "ParseError", "lib", "ChebFilter", "SpectrumBounds", "adaptive_degree", "build_filter",
+    "chebyshev_step_coeffs", "eval_filter_scalar", "initial_degree", "jackson_damping", "lanczos_damping",
+    "Context", "DeviceCsr", "clenshaw_apply", "clenshaw_apply_device", "default_context", "maspmm",
+    "maspmm_device", "CsrMatrix", "fill_gaussian", "fill_rademacher", "parse_matrix_market", "philox_block",
+    "philox_gaussian", "philox_uniform", "read_matrix_market",
+]

@@ -1,0 +1,120 @@
+// Internal definitions shared by the libadp_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "adp.h"
+
+namespace adp {
+
+using index_t = std::int64_t;
+
+// Exceptions inside the library; the C-ABI converts them to adp_status.
+struct Error : std::runtime_error {
+  adp_status code;
+  Error(adp_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(adp_status c, const std::string& m) { throw Error(c, m); }
+
+void set_last_error(const std::string& m);
+
+#define ADP_CUDA(call)                                                                               \
+  do {                                                                                               \
+    cudaError_t err__ = (call);                                                                      \
+    if (err__ != cudaSuccess)                                                                        \
+      ::adp::fail(err__ == cudaErrorMemoryAllocation ? ADP_ERR_OOM : ADP_ERR_CUDA,                   \
+                  std::string(#call) + ": " + cudaGetErrorString(err__));                            \
+  } while (0)
+
+#define ADP_LAUNCH_CHECK() ADP_CUDA(cudaGetLastError())
+
+// Grow-only device scratch buffer.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (ptr) cudaFree(ptr);
+      ptr = nullptr;
+      bytes = 0;
+      if (need) ADP_CUDA(cudaMalloc(&ptr, need));
+      bytes = need;
+    }
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace adp
+
+struct adp_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // where work is queued (own or borrowed)
+  int sm_count = 148;
+  int64_t launches = 0;
+  int panel_cols = 0;  // 0 = automatic
+  adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
+  void* cublas = nullptr;
+  void* cusolver = nullptr;
+};
+
+struct adp_csr {
+  adp_ctx* ctx = nullptr;
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  adp_dtype dtype = ADP_F64;
+  bool rp64 = false;          // int64 row offsets (nnz >= 2^31)
+  void* row_ptr = nullptr;    // int32[n_rows+1] or int64[n_rows+1]
+  int32_t* col_idx = nullptr; // int32[nnz]
+  void* values = nullptr;     // double[nnz] or double2[nnz]
+};
+
+namespace adp {
+
+// ---- kernels (cheb_step.cu) ---------------------------------------------------
+enum class StepMode : int { First = 0, Step = 1, Deg1 = 2, Spmm = 3, SpmmAcc = 4 };
+
+// One launch of the fused Clenshaw step: out = epilogue(A * G, own rows).
+struct StepArgs {
+  const adp_csr* a;
+  const void* gsrc;  // gathered operand (W for Step, Y for First, X for Deg1, B for Spmm)
+  const void* vin;   // Step: V (previous), read
+  const void* yin;   // Step: Y
+  void* out;         // Step/Deg1/Spmm: output rows; First: V
+  void* wout;        // First: W = c_d * Y
+  int64_t ld;        // leading dimension (elements of the scalar type) of gsrc/vin
+  int64_t ld_y;      // leading dimension of yin
+  int64_t ld_out;    // leading dimension of out/wout
+  int64_t q;         // columns
+  int64_t row_begin, row_end;
+  int64_t goff;      // own row of out-row r inside gsrc is r + goff (0 unless halo-extended)
+  double s0, s1, s2, s3;
+};
+void launch_step(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+
+// Layout kernels (layout.cu). Elements are 8 B (f64) or 16 B (c128).
+void launch_colmajor_to_rowmajor(adp_ctx* ctx, const void* src, int64_t n, int64_t q, int64_t lds, void* dst,
+                                 int64_t ldd, int elem_bytes);
+void launch_rowmajor_to_colmajor(adp_ctx* ctx, const void* src, int64_t n, int64_t q, int64_t lds, void* dst,
+                                 int64_t ldd, int elem_bytes);
+void launch_scale_rows(adp_ctx* ctx, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t n, int64_t q,
+                       double s, int elem_bytes);
+void launch_fill_philox(adp_ctx* ctx, double* dst, int64_t n, int64_t q, int64_t ld, uint64_t seed,
+                        uint64_t stream, int kind);
+
+// Host filter helpers (filter_host.cpp).
+std::vector<double> step_coeffs(double alpha, double beta, int k);
+std::vector<double> lanczos_damping(int k, double m);
+std::vector<double> jackson_damping(int k);
+double map_clamped(const adp_filter_info& f, double x, bool* clamped);
+
+}  // namespace adp

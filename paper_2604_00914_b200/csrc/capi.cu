@@ -1,0 +1,482 @@
+// C-ABI implementation of the operator level: context, device CSR, the
+// Clenshaw filter application and maspmm (include/adp.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "adp_internal.hpp"
+
+namespace adp {
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+adp_status guarded(F&& f) {
+  try {
+    f();
+    return ADP_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = std::string("host allocation failed: ") + e.what();
+    return ADP_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return ADP_ERR_RUNTIME;
+  }
+}
+
+size_t elem_bytes(const adp_csr* a) { return a->dtype == ADP_C128 ? 16 : 8; }
+
+// Row-major workspace leading dimension: even number of fp64 columns so every
+// row starts 16-byte aligned; complex rows are already 16-byte elements.
+int64_t ws_ld(const adp_csr* a, int64_t q) { return a->dtype == ADP_C128 ? q : ((q + 1) / 2) * 2; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+void set_device(adp_ctx* ctx) { ADP_CUDA(cudaSetDevice(ctx->device)); }
+
+// Degree after dropping exactly-zero trailing coefficients (cheb_filter.cpp:141-142).
+int effective_degree(const double* coeffs, int degree) {
+  int deg = degree;
+  while (deg > 0 && coeffs[deg] == 0.0) --deg;
+  return deg;
+}
+
+// The device core of clenshaw_apply (cheb_filter.cpp:146-178) on row-major
+// blocks. Y: input (ld_y), out: result (ld_out), w_buf / v_buf: workspaces
+// with leading dimension ld. Degree already reduced.
+void clenshaw_device(adp_ctx* ctx, const adp_csr* a, const double* coeffs, double l1, double l2, int deg,
+                     const void* y, int64_t ld_y, void* out, int64_t ld_out, void* w_buf, void* v_buf, int64_t ld,
+                     int64_t q) {
+  const int eb = static_cast<int>(elem_bytes(a));
+  const int64_t n = a->n_rows;
+  if (deg == 0) {  // f.coeffs[0] * x
+    launch_scale_rows(ctx, y, ld_y, out, ld_out, n, q, coeffs[0], eb);
+    return;
+  }
+  StepArgs s{};
+  s.a = a;
+  s.q = q;
+  s.row_begin = 0;
+  s.row_end = n;
+  s.goff = 0;
+  if (deg == 1) {  // c0 x + c1 (l1 A x + l2 x)
+    s.gsrc = y;
+    s.ld = ld_y;
+    s.ld_y = ld_y;
+    s.out = out;
+    s.ld_out = ld_out;
+    s.s0 = coeffs[0];
+    s.s1 = coeffs[1];
+    s.s2 = l1;
+    s.s3 = l2;
+    launch_step(ctx, StepMode::Deg1, s);
+    return;
+  }
+  // w = c_d y ; v = 2 l1 A w + (2 l2 + c_{d-1}/c_d) w ; swap(v, w)
+  s.gsrc = y;
+  s.ld = ld_y;
+  s.ld_y = ld_y;
+  s.wout = w_buf;
+  s.out = v_buf;
+  s.ld_out = ld;
+  s.s0 = 2.0 * l1;
+  s.s1 = 2.0 * l2 + coeffs[deg - 1] / coeffs[deg];
+  s.s2 = coeffs[deg];
+  launch_step(ctx, StepMode::First, s);
+  void* cur_w = v_buf;
+  void* cur_v = w_buf;
+  s.wout = nullptr;
+  s.yin = y;
+  s.ld = ld;
+  s.ld_y = ld_y;
+  for (int j = deg - 2; j >= 1; --j) {  // v = ((2l1 A w + 2l2 w) - v) + c_j y ; swap
+    s.gsrc = cur_w;
+    s.vin = cur_v;
+    s.out = cur_v;
+    s.ld_out = ld;
+    s.s0 = 2.0 * l1;
+    s.s1 = 2.0 * l2;
+    s.s2 = coeffs[j];
+    launch_step(ctx, StepMode::Step, s);
+    std::swap(cur_w, cur_v);
+  }
+  // v = ((l1 A w + l2 w) - v) + c0 y, written straight to the output
+  s.gsrc = cur_w;
+  s.vin = cur_v;
+  s.out = out;
+  s.ld_out = ld_out;
+  s.s0 = l1;
+  s.s1 = l2;
+  s.s2 = coeffs[0];
+  launch_step(ctx, StepMode::Step, s);
+}
+
+void check_filter_args(const adp_csr* a, const double* coeffs, int32_t k_max, int32_t degree, int64_t x_rows,
+                       int64_t q) {
+  if (!a) fail(ADP_ERR_RUNTIME, "clenshaw_apply: null matrix");
+  if (degree < 0 || degree > k_max) fail(ADP_ERR_CONFIG, "clenshaw_apply: degree out of range");
+  if (!coeffs) fail(ADP_ERR_CONFIG, "clenshaw_apply: null coefficient array");
+  if (x_rows != a->n_cols) fail(ADP_ERR_DIMENSION, "clenshaw_apply: operand row count does not match A");
+  if (a->n_rows != a->n_cols) fail(ADP_ERR_DIMENSION, "clenshaw_apply: operator must be square");
+  if (q < 0) fail(ADP_ERR_DIMENSION, "clenshaw_apply: negative column count");
+}
+
+// host (layout, ld) -> device row-major (ldd), via staging for column-major.
+void upload_block(adp_ctx* ctx, const void* host, int64_t n, int64_t q, int64_t ldh, adp_layout layout, void* dev,
+                  int64_t ldd, void* staging, size_t eb) {
+  if (n == 0 || q == 0) return;
+  if (layout == ADP_ROW_MAJOR) {
+    ADP_CUDA(cudaMemcpy2DAsync(dev, ldd * eb, host, ldh * eb, q * eb, n, cudaMemcpyHostToDevice, ctx->stream));
+    return;
+  }
+  if (ldh == n)
+    ADP_CUDA(cudaMemcpyAsync(staging, host, n * q * eb, cudaMemcpyHostToDevice, ctx->stream));
+  else
+    ADP_CUDA(cudaMemcpy2DAsync(staging, n * eb, host, ldh * eb, n * eb, q, cudaMemcpyHostToDevice, ctx->stream));
+  launch_colmajor_to_rowmajor(ctx, staging, n, q, n, dev, ldd, static_cast<int>(eb));
+}
+
+void download_block(adp_ctx* ctx, const void* dev, int64_t ldd, int64_t n, int64_t q, void* host, int64_t ldh,
+                    adp_layout layout, void* staging, size_t eb) {
+  if (n == 0 || q == 0) return;
+  if (layout == ADP_ROW_MAJOR) {
+    ADP_CUDA(cudaMemcpy2DAsync(host, ldh * eb, dev, ldd * eb, q * eb, n, cudaMemcpyDeviceToHost, ctx->stream));
+    return;
+  }
+  launch_rowmajor_to_colmajor(ctx, dev, n, q, ldd, staging, n, static_cast<int>(eb));
+  if (ldh == n)
+    ADP_CUDA(cudaMemcpyAsync(host, staging, n * q * eb, cudaMemcpyDeviceToHost, ctx->stream));
+  else
+    ADP_CUDA(cudaMemcpy2DAsync(host, ldh * eb, staging, n * eb, n * eb, q, cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+}  // namespace
+
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+}  // namespace adp
+
+using namespace adp;
+
+extern "C" {
+
+int32_t adp_version(void) { return 1; }
+
+const char* adp_last_error_message(void) { return adp::g_last_error.c_str(); }
+
+adp_status adp_ctx_create(int32_t device, adp_ctx** out) {
+  return guarded([&] {
+    int count = 0;
+    ADP_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) fail(ADP_ERR_CONFIG, "adp_ctx_create: no such device");
+    auto* ctx = new adp_ctx;
+    ctx->device = device;
+    try {
+      ADP_CUDA(cudaSetDevice(device));
+      ADP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+      ADP_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+  });
+}
+
+void adp_release_dense_handles(adp_ctx* ctx);  // dense.cu
+
+adp_status adp_ctx_destroy(adp_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    adp_release_dense_handles(ctx);
+    for (auto& b : ctx->ws) b.release();
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+  });
+}
+
+adp_status adp_ctx_set_stream(adp_ctx* ctx, void* stream) {
+  return guarded([&] {
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  });
+}
+
+adp_status adp_ctx_synchronize(adp_ctx* ctx) {
+  return guarded([&] {
+    set_device(ctx);
+    ADP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int64_t adp_ctx_launch_count(const adp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
+  return guarded([&] {
+    if (panel_cols < 0) fail(ADP_ERR_CONFIG, "adp_ctx_set_panel: negative panel width");
+    ctx->panel_cols = panel_cols;
+  });
+}
+
+// csr upload; validation mirrors CsrMatrix::validate (csr_matrix.hpp:101-116).
+adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                          const int64_t* col_idx, const void* values, adp_dtype dtype, adp_csr** out) {
+  return guarded([&] {
+    if (n_rows < 0 || n_cols < 0) fail(ADP_ERR_DIMENSION, "negative matrix size");
+    if (n_cols > std::numeric_limits<int32_t>::max() || n_rows > std::numeric_limits<int32_t>::max())
+      fail(ADP_ERR_DIMENSION, "adp_csr_create: dimension exceeds int32 column indexing");
+    if (dtype != ADP_F64 && dtype != ADP_C128) fail(ADP_ERR_CONFIG, "adp_csr_create: unknown dtype");
+    if (row_ptr[0] != 0) fail(ADP_ERR_DIMENSION, "row_ptr endpoints mismatch");
+    const int64_t nnz = row_ptr[n_rows];
+    std::vector<int32_t> col32(static_cast<size_t>(nnz));
+    for (int64_t r = 0; r < n_rows; ++r) {
+      if (row_ptr[r + 1] < row_ptr[r]) fail(ADP_ERR_DIMENSION, "row_ptr not non-decreasing");
+      for (int64_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) {
+        if (col_idx[k] < 0 || col_idx[k] >= n_cols) fail(ADP_ERR_DIMENSION, "column index out of range");
+        if (k > row_ptr[r] && col_idx[k] <= col_idx[k - 1])
+          fail(ADP_ERR_DIMENSION, "columns not strictly increasing within a row");
+        col32[k] = static_cast<int32_t>(col_idx[k]);
+      }
+    }
+    set_device(ctx);
+    auto* a = new adp_csr;
+    a->ctx = ctx;
+    a->n_rows = n_rows;
+    a->n_cols = n_cols;
+    a->nnz = nnz;
+    a->dtype = dtype;
+    a->rp64 = nnz > std::numeric_limits<int32_t>::max();
+    const size_t eb = dtype == ADP_C128 ? 16 : 8;
+    try {
+      const size_t rp_bytes = (n_rows + 1) * (a->rp64 ? 8 : 4);
+      ADP_CUDA(cudaMalloc(&a->row_ptr, rp_bytes));
+      ADP_CUDA(cudaMalloc(reinterpret_cast<void**>(&a->col_idx), std::max<size_t>(nnz, 1) * 4));
+      ADP_CUDA(cudaMalloc(&a->values, std::max<size_t>(nnz, 1) * eb));
+      if (a->rp64) {
+        ADP_CUDA(cudaMemcpy(a->row_ptr, row_ptr, rp_bytes, cudaMemcpyHostToDevice));
+      } else {
+        std::vector<int32_t> rp32(n_rows + 1);
+        for (int64_t r = 0; r <= n_rows; ++r) rp32[r] = static_cast<int32_t>(row_ptr[r]);
+        ADP_CUDA(cudaMemcpy(a->row_ptr, rp32.data(), rp_bytes, cudaMemcpyHostToDevice));
+      }
+      if (nnz) {
+        ADP_CUDA(cudaMemcpy(a->col_idx, col32.data(), nnz * 4, cudaMemcpyHostToDevice));
+        ADP_CUDA(cudaMemcpy(a->values, values, nnz * eb, cudaMemcpyHostToDevice));
+      }
+    } catch (...) {
+      cudaFree(a->row_ptr);
+      cudaFree(a->col_idx);
+      cudaFree(a->values);
+      delete a;
+      throw;
+    }
+    *out = a;
+  });
+}
+
+adp_status adp_csr_destroy(adp_csr* a) {
+  return guarded([&] {
+    if (!a) return;
+    cudaSetDevice(a->ctx->device);
+    cudaStreamSynchronize(a->ctx->stream);
+    cudaFree(a->row_ptr);
+    cudaFree(a->col_idx);
+    cudaFree(a->values);
+    delete a;
+  });
+}
+
+adp_status adp_csr_info(const adp_csr* a, int64_t* n_rows, int64_t* n_cols, int64_t* nnz, int32_t* dtype) {
+  return guarded([&] {
+    if (n_rows) *n_rows = a->n_rows;
+    if (n_cols) *n_cols = a->n_cols;
+    if (nnz) *nnz = a->nnz;
+    if (dtype) *dtype = a->dtype;
+  });
+}
+
+adp_status adp_filter_apply_device(adp_ctx* ctx, const adp_csr* a, const double* coeffs, int32_t k_max, double l1,
+                                   double l2, int32_t degree, const void* dx, int64_t x_rows, int64_t ldx, int64_t q,
+                                   void* dy, int64_t ldy, int64_t* spmv_count) {
+  return guarded([&] {
+    check_filter_args(a, coeffs, k_max, degree, x_rows, q);
+    if (q == 0) return;
+    if (ldx < q || ldy < q) fail(ADP_ERR_DIMENSION, "clenshaw_apply: leading dimension smaller than q");
+    set_device(ctx);
+    const int deg = effective_degree(coeffs, degree);
+    if (spmv_count) *spmv_count += static_cast<int64_t>(deg) * q;
+    const size_t eb = elem_bytes(a);
+    const int64_t n = a->n_rows;
+    const int64_t ld = ws_ld(a, q);
+    // Operands that already satisfy the kernel contract are used in place:
+    // 16-byte aligned rows and no padding column that the last vector would
+    // touch (q even for fp64).
+    const bool pad_free = a->dtype == ADP_C128 || q % 2 == 0;
+    const bool x_ok = pad_free && aligned16(dx) && (a->dtype == ADP_C128 || ldx % 2 == 0);
+    const bool y_ok = pad_free && aligned16(dy) && (a->dtype == ADP_C128 || ldy % 2 == 0);
+    const size_t blk = static_cast<size_t>(n) * ld * eb;
+    const void* yin = dx;
+    int64_t ld_y = ldx;
+    if (!x_ok) {
+      void* ybuf = ctx->ws[1].get(blk);
+      ADP_CUDA(cudaMemsetAsync(ybuf, 0, blk, ctx->stream));
+      ADP_CUDA(cudaMemcpy2DAsync(ybuf, ld * eb, dx, ldx * eb, q * eb, n, cudaMemcpyDeviceToDevice, ctx->stream));
+      yin = ybuf;
+      ld_y = ld;
+    }
+    void* wbuf = ctx->ws[2].get(blk);
+    void* vbuf = ctx->ws[3].get(blk);
+    if (y_ok) {
+      clenshaw_device(ctx, a, coeffs, l1, l2, deg, yin, ld_y, dy, ldy, wbuf, vbuf, ld, q);
+    } else {
+      void* obuf = ctx->ws[4].get(blk);
+      clenshaw_device(ctx, a, coeffs, l1, l2, deg, yin, ld_y, obuf, ld, wbuf, vbuf, ld, q);
+      ADP_CUDA(cudaMemcpy2DAsync(dy, ldy * eb, obuf, ld * eb, q * eb, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  });
+}
+
+adp_status adp_filter_apply(adp_ctx* ctx, const adp_csr* a, const double* coeffs, int32_t k_max, double l1,
+                            double l2, int32_t degree, const void* x, int64_t x_rows, int64_t ldx, int64_t q,
+                            adp_layout layout, void* y, int64_t ldy, int64_t* spmv_count) {
+  return guarded([&] {
+    check_filter_args(a, coeffs, k_max, degree, x_rows, q);
+    if (q == 0) return;
+    const int64_t n = a->n_rows;
+    if (layout == ADP_COL_MAJOR ? (ldx < n || ldy < n) : (ldx < q || ldy < q))
+      fail(ADP_ERR_DIMENSION, "clenshaw_apply: leading dimension too small");
+    set_device(ctx);
+    const int deg = effective_degree(coeffs, degree);
+    if (spmv_count) *spmv_count += static_cast<int64_t>(deg) * q;
+    const size_t eb = elem_bytes(a);
+    const int64_t ld = ws_ld(a, q);
+    const size_t blk = static_cast<size_t>(n) * ld * eb;
+    void* staging = ctx->ws[0].get(static_cast<size_t>(n) * q * eb);
+    void* ybuf = ctx->ws[1].get(blk);
+    void* wbuf = ctx->ws[2].get(blk);
+    void* vbuf = ctx->ws[3].get(blk);
+    if (ld != q) ADP_CUDA(cudaMemsetAsync(ybuf, 0, blk, ctx->stream));
+    upload_block(ctx, x, n, q, ldx, layout, ybuf, ld, staging, eb);
+    // The result lands in the V workspace of the last step (in place), then
+    // leaves through the staging buffer.
+    void* obuf = deg >= 2 ? ((deg % 2 == 0) ? wbuf : vbuf) : vbuf;
+    clenshaw_device(ctx, a, coeffs, l1, l2, deg, ybuf, ld, obuf, ld, wbuf, vbuf, ld, q);
+    download_block(ctx, obuf, ld, n, q, y, ldy, layout, staging, eb);
+    ADP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+adp_status adp_spmm_device(adp_ctx* ctx, const adp_csr* a, const void* db, int64_t b_rows, int64_t ldb, int64_t k,
+                           void* dc, int64_t ldc, int32_t accumulate) {
+  return guarded([&] {
+    if (b_rows != a->n_cols) fail(ADP_ERR_DIMENSION, "maspmm: shape mismatch");
+    if (k == 0) return;
+    if (ldb < k || ldc < k) fail(ADP_ERR_DIMENSION, "maspmm: leading dimension smaller than k");
+    set_device(ctx);
+    const size_t eb = elem_bytes(a);
+    const bool pad_free = a->dtype == ADP_C128 || k % 2 == 0;
+    const bool b_ok = pad_free && aligned16(db) && (a->dtype == ADP_C128 || ldb % 2 == 0);
+    const bool c_ok = pad_free && aligned16(dc) && (a->dtype == ADP_C128 || ldc % 2 == 0);
+    const int64_t ld = ws_ld(a, k);
+    const void* bsrc = db;
+    int64_t ld_b = ldb;
+    if (!b_ok) {
+      const size_t blk = static_cast<size_t>(a->n_cols) * ld * eb;
+      void* bbuf = ctx->ws[1].get(blk);
+      ADP_CUDA(cudaMemsetAsync(bbuf, 0, blk, ctx->stream));
+      ADP_CUDA(cudaMemcpy2DAsync(bbuf, ld * eb, db, ldb * eb, k * eb, a->n_cols, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+      bsrc = bbuf;
+      ld_b = ld;
+    }
+    void* cdst = dc;
+    int64_t ld_c = ldc;
+    const size_t cblk = static_cast<size_t>(a->n_rows) * ld * eb;
+    if (!c_ok) {
+      cdst = ctx->ws[4].get(cblk);
+      ld_c = ld;
+      if (accumulate) {
+        ADP_CUDA(cudaMemsetAsync(cdst, 0, cblk, ctx->stream));
+        ADP_CUDA(cudaMemcpy2DAsync(cdst, ld * eb, dc, ldc * eb, k * eb, a->n_rows, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+      }
+    }
+    StepArgs s{};
+    s.a = a;
+    s.gsrc = bsrc;
+    s.ld = ld_b;
+    s.ld_y = ld_b;
+    s.out = cdst;
+    s.ld_out = ld_c;
+    s.q = k;
+    s.row_begin = 0;
+    s.row_end = a->n_rows;
+    launch_step(ctx, accumulate ? StepMode::SpmmAcc : StepMode::Spmm, s);
+    if (!c_ok)
+      ADP_CUDA(cudaMemcpy2DAsync(dc, ldc * eb, cdst, ld * eb, k * eb, a->n_rows, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+  });
+}
+
+adp_status adp_spmm(adp_ctx* ctx, const adp_csr* a, const void* b, int64_t b_rows, int64_t ldb, int64_t k,
+                    adp_layout layout, void* c, int64_t ldc, int32_t accumulate) {
+  return guarded([&] {
+    if (b_rows != a->n_cols) fail(ADP_ERR_DIMENSION, "maspmm: shape mismatch");
+    if (k == 0) return;
+    set_device(ctx);
+    const size_t eb = elem_bytes(a);
+    const int64_t ld = ws_ld(a, k);
+    const int64_t nb = a->n_cols, nc = a->n_rows;
+    void* staging = ctx->ws[0].get(static_cast<size_t>(std::max(nb, nc)) * k * eb);
+    void* bbuf = ctx->ws[1].get(static_cast<size_t>(nb) * ld * eb);
+    void* cbuf = ctx->ws[4].get(static_cast<size_t>(nc) * ld * eb);
+    if (ld != k) {
+      ADP_CUDA(cudaMemsetAsync(bbuf, 0, static_cast<size_t>(nb) * ld * eb, ctx->stream));
+      ADP_CUDA(cudaMemsetAsync(cbuf, 0, static_cast<size_t>(nc) * ld * eb, ctx->stream));
+    }
+    upload_block(ctx, b, nb, k, ldb, layout, bbuf, ld, staging, eb);
+    if (accumulate) upload_block(ctx, c, nc, k, ldc, layout, cbuf, ld, staging, eb);
+    StepArgs s{};
+    s.a = a;
+    s.gsrc = bbuf;
+    s.ld = ld;
+    s.ld_y = ld;
+    s.out = cbuf;
+    s.ld_out = ld;
+    s.q = k;
+    s.row_begin = 0;
+    s.row_end = nc;
+    launch_step(ctx, accumulate ? StepMode::SpmmAcc : StepMode::Spmm, s);
+    download_block(ctx, cbuf, ld, nc, k, c, ldc, layout, staging, eb);
+    ADP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+adp_status adp_fill_gaussian_device(adp_ctx* ctx, double* d_out, int64_t n, int64_t q, int64_t ld, uint64_t seed,
+                                    uint64_t stream) {
+  return guarded([&] {
+    set_device(ctx);
+    launch_fill_philox(ctx, d_out, n, q, ld, seed, stream, 0);
+  });
+}
+
+adp_status adp_fill_rademacher_device(adp_ctx* ctx, double* d_out, int64_t n, int64_t q, int64_t ld,
+                                      uint64_t seed, uint64_t stream) {
+  return guarded([&] {
+    set_device(ctx);
+    launch_fill_philox(ctx, d_out, n, q, ld, seed, stream, 1);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path through the C-ABI vs the pinned CPU oracle.
+
+The bar is BITWISE equality: the kernel accumulates every
+output element in ascending column order with unfused IEEE multiplies and adds
+in the reference's expression order, exactly like the reference's maspmm +
+Eigen array updates (proj/include/adapoly/tiled_matrix.hpp:205,
+proj/src/cheb_filter.cpp:162-177). The north-star tolerance (1e-12 relative
+Frobenius per degree) is therefore checked as exact equality.
+"""
+import numpy as np
+import pytest
+
+import paper_2604_00914_b200 as adp
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = adp.Context(0)
+    yield c
+    c.close()
+
+
+def dev(ctx, a):
+    return adp.DeviceCsr(adp.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values), ctx)
+
+
+def same_filter(orc, a, b, bounds, k, m=0.5):
+    return adp.build_filter(a, b, bounds, k, m), orc.build_filter(a, b, bounds, k, m)
+
+
+def assert_bitwise(got, want):
+    assert got.shape == want.shape
+    if not np.array_equal(got, want):
+        diff = np.abs(got - want)
+        i = np.unravel_index(np.argmax(diff), diff.shape)
+        rel = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300)
+        raise AssertionError(f"not bitwise equal: max |diff| {diff.max():.3e} at {i}, rel fro {rel:.3e}")
+
+
+# ------------------------------------------------------------ golden files ---
+def test_golden_fixtures(ctx, golden_dir):
+    z = np.load(f"{golden_dir}/clenshaw_golden.npz")
+    for name in ("laplacian2d_30", "arrow_ints", "banded_mixed"):
+        fx = np.load(f"{golden_dir}/fixture_{name}.npz")
+        a = adp.DeviceCsr(adp.CsrMatrix(int(fx["n_rows"]), int(fx["n_cols"]), fx["row_ptr"], fx["col_idx"],
+                                        fx["values"]), ctx)
+        l1, l2, kmax, lo, hi, b0, b1 = z[f"{name}/l1l2"]
+        f = adp.build_filter(lo, hi, (b0, b1), int(kmax), 0.5)
+        assert np.array_equal(f.coeffs, z[f"{name}/coeffs"])
+        for d in (0, 1, 2, 3, 17, 40):
+            assert_bitwise(adp.clenshaw_apply(f, a, z[f"{name}/x"], d), z[f"{name}/deg{d}"])
+
+
+# --------------------------------------------- reference hot-path test cases ---
+@pytest.mark.parametrize("q", [1, 2, 3, 5, 6, 8, 16, 17, 30, 33, 64, 65, 128, 130, 256, 384, 520, 1024])
+def test_clenshaw_bitwise_widths(ctx, orc, q):
+    # random_symmetric(80, 0.1, 31) -- the matrix of test_cheb_filter.cpp:225-240
+    a = orc.random_symmetric(80, 0.1, 31)
+    spec = np.linalg.eigvalsh(a.to_dense())
+    f, g = same_filter(orc, spec[10], spec[50], (spec[0] - 0.1, spec[-1] + 0.1), 60)
+    da, t = dev(ctx, a), orc.Tiled(a, 16, 8)
+    x = orc.fill_gaussian(80, q, 77, 3)
+    for degree in (0, 1, 2, 3, 25, 60):
+        s1, s2 = [0], [0]
+        assert_bitwise(adp.clenshaw_apply(f, da, x, degree, s1), orc.clenshaw_apply(g, t, x, degree, s2))
+        assert s1[0] == s2[0]
+
+
+def test_clenshaw_diagonal_and_identity(ctx, orc):
+    rng = orc.MT19937_64(3)
+    diag = [rng.uniform(-0.95, 0.95) for _ in range(40)]
+    a = orc.make_diag(diag)
+    f, g = same_filter(orc, -0.3, 0.5, (-1.0, 1.0), 35)
+    x = orc.fill_gaussian(40, 3, 5, 1)
+    for d in (1, 2, 7, 35):
+        assert_bitwise(adp.clenshaw_apply(f, dev(ctx, a), x, d), orc.clenshaw_apply(g, orc.Tiled(a, 16, 4), x, d))
+    # full-interval filter returns X exactly with no products (test_cheb_filter.cpp:211-223)
+    a = orc.random_symmetric(30, 0.2, 9)
+    f = adp.build_filter(-40.0, 40.0, (-40.0, 40.0), 20, 0.5)
+    x = orc.fill_gaussian(30, 4, 2, 0)
+    spmv = [0]
+    assert np.array_equal(adp.clenshaw_apply(f, dev(ctx, a), x, 20, spmv), x) and spmv[0] == 0
+
+
+def test_clenshaw_trailing_zero_and_accounting(ctx, orc):
+    a = orc.make_diag([0.1, -0.4, 0.7, 0.2])
+    f, g = same_filter(orc, -0.5, 0.5, (-1.0, 1.0), 5, 0.0)
+    f.coeffs = g.coeffs = np.array([0.3, 0.5, 0.2, 0.0, 0.0, 0.0])
+    x = orc.fill_gaussian(4, 2, 1, 0)
+    s = [0]
+    assert_bitwise(adp.clenshaw_apply(f, dev(ctx, a), x, 5, s), orc.clenshaw_apply(g, orc.Tiled(a, 2, 2), x, 5))
+    assert s[0] == 4
+    a = orc.random_symmetric(24, 0.3, 12)
+    f = adp.build_filter(-2.0, 5.0, (-30.0, 30.0), 12, 0.5)
+    x = orc.fill_gaussian(24, 5, 8, 2)
+    s = [0]
+    da = dev(ctx, a)
+    adp.clenshaw_apply(f, da, x, 12, s)
+    adp.clenshaw_apply(f, da, x, 3, s)
+    assert s[0] == 75
+    with pytest.raises(adp.ConfigError):
+        adp.clenshaw_apply(f, da, x, 13)
+    with pytest.raises(adp.ConfigError):
+        adp.clenshaw_apply(f, da, x, -1)
+    with pytest.raises(adp.DimensionError):
+        adp.clenshaw_apply(f, da, x[:20], 3)
+
+
+def test_acceptance5_matrices_bitwise(ctx, orc):
+    for n in (60, 130, 200):
+        a = orc.random_symmetric(n, 0.08, 600 + n)
+        ev = np.linalg.eigvalsh(a.to_dense())
+        f, g = same_filter(orc, ev[n // 4], ev[n // 2], (ev[0] - 0.1, ev[-1] + 0.1), 60)
+        x = orc.fill_gaussian(n, 5, n, 1)
+        for d in (10, 35, 60):
+            assert_bitwise(adp.clenshaw_apply(f, dev(ctx, a), x, d), orc.clenshaw_apply(g, orc.Tiled(a, 32, 8), x, d))
+
+
+# ------------------------------------------------------------------ maspmm ---
+def test_spmm_acceptance4_bitwise(ctx, orc, golden_dir):
+    mats = []
+    rng = orc.MT19937_64(4242)
+    for i in range(20):
+        n = 50 + rng() % 251
+        density = 0.01 + 0.09 * rng.uniform(0.0, 1.0)
+        if i % 5 == 4:
+            mats.append(orc.random_csr(n, 40 + rng() % 100, density, 100 + i))
+        else:
+            mats.append(orc.random_symmetric(n, density, 100 + i))
+    for name in ("laplacian2d_30", "arrow_ints", "banded_mixed"):
+        z = np.load(f"{golden_dir}/fixture_{name}.npz")
+        mats.append(orc.Csr(int(z["n_rows"]), int(z["n_cols"]), z["row_ptr"], z["col_idx"], z["values"]))
+    cases = 0
+    for a in mats:
+        da = dev(ctx, a)
+        for k in (1, 8, 32, 128):
+            b = orc.fill_gaussian(a.n_cols, k, 31 + cases, 0)
+            want = orc.maspmm(orc.Tiled(a, 256, 64), b)
+            assert_bitwise(adp.maspmm(da, b), want)
+            c0 = orc.fill_gaussian(a.n_rows, k, 5, 5)
+            assert_bitwise(adp.maspmm(da, b, c0), orc.maspmm(orc.Tiled(a, 7, 8), b, c0))
+            cases += 1
+    assert cases == 92
+
+
+def test_spmm_errors(ctx, orc):
+    a = dev(ctx, orc.make_diag(np.ones(6)))
+    with pytest.raises(adp.DimensionError):
+        adp.maspmm(a, np.zeros((5, 3)))
+    assert adp.maspmm(a, np.zeros((6, 0))).shape == (6, 0)
+
+
+# ------------------------------------------------------------- device API ---
+def test_device_api_layouts(ctx, orc):
+    a = orc.random_symmetric(300, 0.03, 7)
+    spec = np.linalg.eigvalsh(a.to_dense())
+    f, g = same_filter(orc, spec[100], spec[140], (spec[0] - 0.1, spec[-1] + 0.1), 30)
+    da, t = dev(ctx, a), orc.Tiled(a, 256, 64)
+    for q, ldx, ldy, off in [(64, 64, 64, 0), (5, 5, 7, 0), (6, 10, 6, 1), (33, 40, 34, 0), (128, 130, 128, 0)]:
+        x = orc.fill_gaussian(300, q, q, 0)
+        xt = torch.zeros(300 * ldx + 2, dtype=torch.float64, device="cuda")
+        xv = xt[off:off + 300 * ldx].view(300, ldx)[:, :q]
+        xv.copy_(torch.from_numpy(np.ascontiguousarray(x)))
+        yt = torch.full((300 * ldy + 2,), float("nan"), dtype=torch.float64, device="cuda")
+        yv = yt[off:off + 300 * ldy].view(300, ldy)[:, :q]
+        for d in (0, 1, 2, 9, 30):
+            adp.clenshaw_apply_device(f, da, xv, d, out=yv)
+            torch.cuda.synchronize()
+            assert_bitwise(yv.cpu().numpy(), orc.clenshaw_apply(g, t, x, d))
+        if ldy > q:  # padding columns of the caller's buffer are untouched
+            assert torch.isnan(yt[off:off + 300 * ldy].view(300, ldy)[:, q:]).all()
+
+
+def test_host_row_major_layout(ctx, orc):
+    a = orc.random_symmetric(120, 0.05, 3)
+    f, g = same_filter(orc, -0.5, 0.2, (-8.0, 8.0), 20)
+    x = orc.fill_gaussian(120, 7, 1, 0)
+    want = orc.clenshaw_apply(g, orc.Tiled(a, 256, 64), x, 20)
+    assert_bitwise(adp.clenshaw_apply(f, dev(ctx, a), np.ascontiguousarray(x), 20, layout="row"), want)
+
+
+def test_bitwise_deterministic_repeat(ctx, orc):
+    a = orc.random_csr(500, 500, 0.02, 77)
+    da = dev(ctx, a)
+    f = adp.build_filter(-0.5, 0.5, (-10.0, 10.0), 50, 0.5)
+    x = orc.fill_gaussian(500, 17, 4, 2)
+    r1 = adp.clenshaw_apply(f, da, x, 50)
+    r2 = adp.clenshaw_apply(f, da, x, 50)
+    assert np.array_equal(r1, r2)
+
+
+def test_launch_count_is_degree(ctx, orc):
+    a = orc.random_symmetric(100, 0.05, 1)
+    f = adp.build_filter(-0.5, 0.5, (-10.0, 10.0), 40, 0.5)
+    x = torch.zeros(100, 64, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    n0 = ctx.launch_count
+    adp.clenshaw_apply_device(f, dev(ctx, a), x, 40, out=y)
+    assert ctx.launch_count - n0 == 40  # one fused kernel per degree step
+
+
+# --------------------------------------------------------------- complex ---
+def random_hermitian(n, density, seed):
+    rng = np.random.default_rng(seed)
+    m = rng.random((n, n)) < density
+    m = np.triu(m)
+    vals = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = np.where(m, vals, 0)
+    h = h + np.conj(np.triu(h, 1)).T
+    h[np.diag_indices(n)] = h[np.diag_indices(n)].real
+    r, c = np.nonzero(h)
+    return adp.CsrMatrix.from_triplets(n, n, r, c, h[r, c])
+
+
+def test_complex_bitwise_vs_oracle(ctx, orc):
+    for n, q in [(90, 3), (150, 16), (200, 40), (256, 130)]:
+        h = random_hermitian(n, 0.05, n)
+        oh = orc.Csr(h.n_rows, h.n_cols, h.row_ptr, h.col_idx, h.values)
+        ev = np.linalg.eigvalsh(h.to_dense())
+        f, g = same_filter(orc, ev[n // 3], ev[n // 2], (ev[0] - 0.1, ev[-1] + 0.1), 40)
+        rng = np.random.default_rng(q)
+        x = np.asfortranarray(rng.standard_normal((n, q)) + 1j * rng.standard_normal((n, q)))
+        da, t = adp.DeviceCsr(h, ctx), orc.Tiled(oh, 256, 64)
+        for d in (0, 1, 2, 5, 40):
+            assert_bitwise(adp.clenshaw_apply(f, da, x, d), orc.clenshaw_apply(g, t, x, d))
+
+
+# ------------------------------------------------------- full-size configs ---
+def test_config1_full_size_bitwise(ctx, orc):
+    from paper_2604_00914_b200 import configs
+
+    cfg = configs.CONFIGS["c1"]
+    a = cfg.operator()
+    k = configs.filter_degree(cfg)
+    f, g = same_filter(orc, cfg.window[0], cfg.window[1], cfg.bounds, int(np.ceil(2.5 * k)))
+    x = orc.fill_gaussian(a.n_rows, cfg.q, 0, 0)
+    oa = orc.Csr(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)
+    got = adp.clenshaw_apply(f, adp.DeviceCsr(a, ctx), x, k)
+    assert_bitwise(got, orc.clenshaw_apply(g, orc.Tiled(oa, 256, 64), x, k))
+
+
+@pytest.mark.slow
+def test_config2_full_size_bitwise_low_degree(ctx, orc):
+    # n = 1e6, q = 256 (2 GB per block): a few degree steps vs the oracle, bitwise, plus repeatability.
+    from paper_2604_00914_b200 import configs
+
+    cfg = configs.CONFIGS["c2"]
+    a = cfg.operator()
+    f, g = same_filter(orc, cfg.window[0], cfg.window[1], cfg.bounds, 40)
+    x = orc.fill_gaussian(a.n_rows, cfg.q, 0, 0)
+    oa = orc.Csr(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)
+    da = adp.DeviceCsr(a, ctx)
+    got = adp.clenshaw_apply(f, da, x, 4)
+    assert_bitwise(got, orc.clenshaw_apply(g, orc.Tiled(oa, 256, 64), x, 4))
+    assert np.array_equal(adp.clenshaw_apply(f, da, x, 4), got)
