@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--panel", type=int, default=0)
+    p.add_argument("--variant", type=int, default=0)
     return p.parse_args()
 
 
@@ -221,6 +222,8 @@ def run_ours(args):
     ctx = adp.Context(device)
     if args.panel:
         ctx.set_panel(args.panel)
+    if args.variant:
+        ctx.set_tuning(args.variant)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream)
     da = adp.DeviceCsr(a, ctx)

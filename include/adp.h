@@ -63,13 +63,22 @@ int32_t adp_version(void);
 const char* adp_last_error_message(void);
 adp_status adp_ctx_create(int32_t device, adp_ctx** out);
 adp_status adp_ctx_destroy(adp_ctx* ctx);
-/* Run all subsequent work of ctx on an existing cudaStream_t (e.g. torch's). 0 = ctx's own stream. */
+/* Run all subsequent work of ctx on an existing cudaStream_t (e.g. torch's current
+ * stream); NULL is the legacy default stream, as in any CUDA launch. */
 adp_status adp_ctx_set_stream(adp_ctx* ctx, void* cuda_stream);
+/* The non-blocking stream the context created for itself (its initial stream). */
+void* adp_ctx_own_stream(const adp_ctx* ctx);
 adp_status adp_ctx_synchronize(adp_ctx* ctx);
 /* Number of kernels this library has launched on ctx (instrumentation for bench.py). */
 int64_t adp_ctx_launch_count(const adp_ctx* ctx);
 /* Kernel tuning knobs (0 = automatic): columns per warp task (panel width). */
 adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
+/* Kernel tuning variant of the fused step kernel (0 = automatic). */
+adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant);
+/* Tile-kernel knobs (0 = default): 16-byte vectors per lane per panel (1-4),
+ * shared-memory pipeline stages, KiB per stage, resident CTAs per SM. */
+adp_status adp_ctx_set_tile_config(adp_ctx* ctx, int32_t chunks, int32_t stages, int32_t stage_kib,
+                                   int32_t ctas_per_sm);
 
 /* -------------------------------------------------------------- operator -- */
 /* Upload a CSR matrix (CsrMatrix, include/adapoly/csr_matrix.hpp:22-117: int64

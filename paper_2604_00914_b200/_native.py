@@ -76,9 +76,12 @@ SIGNATURES = {
     "adp_ctx_create": (I32, [I32, P]),
     "adp_ctx_destroy": (I32, [P]),
     "adp_ctx_set_stream": (I32, [P, P]),
+    "adp_ctx_own_stream": (P, [P]),
     "adp_ctx_synchronize": (I32, [P]),
     "adp_ctx_launch_count": (I64, [P]),
     "adp_ctx_set_panel": (I32, [P, I32]),
+    "adp_ctx_set_tuning": (I32, [P, I32]),
+    "adp_ctx_set_tile_config": (I32, [P, I32, I32, I32, I32]),
     "adp_csr_create": (I32, [P, I64, I64, P, P, P, I32, P]),
     "adp_csr_destroy": (I32, [P]),
     "adp_csr_info": (I32, [P, P, P, P, P]),

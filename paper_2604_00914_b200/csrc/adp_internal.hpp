@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -63,10 +64,32 @@ struct adp_ctx {
   int sm_count = 148;
   int64_t launches = 0;
   int panel_cols = 0;  // 0 = automatic
+  int variant = 0;     // kernel tuning variant (0 = automatic; 1-7 one-row-per-warp kernel; 11-15 pipelined)
+  int pipe_variant = 0;  // derived: variant - 10 for the pipelined row kernel
+  // tile kernel knobs (0 = default): chunks per lane, pipeline stages, stage KiB, CTAs per SM
+  int tile_ch = 0, tile_stages = 0, tile_stage_kb = 0, tile_ctas = 0;
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;
   void* cusolver = nullptr;
 };
+
+namespace adp {
+constexpr int64_t kMaxTileRows = 64;
+constexpr int64_t kMaxTileDistinct = 256;  // = 32 lanes x kMaxDPerLane (cheb_tile.cu)
+
+// Row tiling of a CSR operator for one (panel width, stage size) pair (tiling.cpp).
+struct Tiling {
+  int64_t panel_bytes = 0, stage_bytes = 0;
+  bool ok = false;
+  int64_t n_tiles = 0, max_rows = 0, distinct = 0;
+  void* d_tile_row = nullptr;   // int32[T+1]
+  void* d_tile_dptr = nullptr;  // int64[T+1]
+  void* d_tile_blob = nullptr;  // int64[T+1] byte offsets into d_blob
+  void* d_dcol = nullptr;       // int32[distinct]
+  void* d_blob = nullptr;       // per-tile metadata blobs
+  ~Tiling();
+};
+}  // namespace adp
 
 struct adp_csr {
   adp_ctx* ctx = nullptr;
@@ -76,6 +99,11 @@ struct adp_csr {
   void* row_ptr = nullptr;    // int32[n_rows+1] or int64[n_rows+1]
   int32_t* col_idx = nullptr; // int32[nnz]
   void* values = nullptr;     // double[nnz] or double2[nnz]
+  // host copies for the tiling preprocessing
+  std::vector<int64_t> h_row_ptr;
+  std::vector<int32_t> h_col;
+  void* h_values = nullptr;  // malloc'd copy of the values
+  std::vector<std::unique_ptr<adp::Tiling>> tilings;
 };
 
 namespace adp {
@@ -110,6 +138,15 @@ void launch_scale_rows(adp_ctx* ctx, const void* src, int64_t lds, void* dst, in
                        double s, int elem_bytes);
 void launch_fill_philox(adp_ctx* ctx, double* dst, int64_t n, int64_t q, int64_t ld, uint64_t seed,
                         uint64_t stream, int kind);
+
+// Tiling (tiling.cpp) and the TMA-pipelined tile kernel (cheb_tile.cu).
+int64_t tile_blob_bytes(int64_t rows, int64_t nnz_t, int64_t val_bytes);
+const Tiling* get_tiling(adp_csr* a, int64_t panel_bytes, int64_t stage_bytes);
+// Launches the tiled kernel for the step; returns false if the operator cannot
+// be tiled for this width (the caller then uses the row kernel).
+bool launch_step_tiled(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+// The persistent software-pipelined row kernel (cheb_row.cu), default for wide blocks.
+bool launch_step_row(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 
 // Host filter helpers (filter_host.cpp).
 std::vector<double> step_coeffs(double alpha, double beta, int k);

@@ -209,9 +209,11 @@ adp_status adp_ctx_destroy(adp_ctx* ctx) {
 
 adp_status adp_ctx_set_stream(adp_ctx* ctx, void* stream) {
   return guarded([&] {
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    ctx->stream = static_cast<cudaStream_t>(stream);
   });
 }
+
+void* adp_ctx_own_stream(const adp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->own_stream) : nullptr; }
 
 adp_status adp_ctx_synchronize(adp_ctx* ctx) {
   return guarded([&] {
@@ -226,6 +228,28 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
   return guarded([&] {
     if (panel_cols < 0) fail(ADP_ERR_CONFIG, "adp_ctx_set_panel: negative panel width");
     ctx->panel_cols = panel_cols;
+  });
+}
+
+adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
+  return guarded([&] {
+    if (variant < 0 || (variant > 7 && variant < 11) || variant > 15)
+      fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
+    ctx->variant = variant;
+    ctx->pipe_variant = variant > 10 ? variant - 10 : 0;
+  });
+}
+
+adp_status adp_ctx_set_tile_config(adp_ctx* ctx, int32_t chunks, int32_t stages, int32_t stage_kib,
+                                   int32_t ctas_per_sm) {
+  return guarded([&] {
+    if (chunks < 0 || chunks > 4 || stages < 0 || stages > 8 || stage_kib < 0 || stage_kib > 220 ||
+        ctas_per_sm < 0 || ctas_per_sm > 4)
+      fail(ADP_ERR_CONFIG, "adp_ctx_set_tile_config: knob out of range");
+    ctx->tile_ch = chunks;
+    ctx->tile_stages = stages;
+    ctx->tile_stage_kb = stage_kib;
+    ctx->tile_ctas = ctas_per_sm;
   });
 }
 
@@ -274,7 +298,13 @@ adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const in
         ADP_CUDA(cudaMemcpy(a->col_idx, col32.data(), nnz * 4, cudaMemcpyHostToDevice));
         ADP_CUDA(cudaMemcpy(a->values, values, nnz * eb, cudaMemcpyHostToDevice));
       }
+      a->h_row_ptr.assign(row_ptr, row_ptr + n_rows + 1);
+      a->h_col = std::move(col32);
+      a->h_values = std::malloc(std::max<size_t>(nnz, 1) * eb);
+      if (!a->h_values) throw std::bad_alloc();
+      if (nnz) std::memcpy(a->h_values, values, nnz * eb);
     } catch (...) {
+      std::free(a->h_values);
       cudaFree(a->row_ptr);
       cudaFree(a->col_idx);
       cudaFree(a->values);
@@ -293,6 +323,7 @@ adp_status adp_csr_destroy(adp_csr* a) {
     cudaFree(a->row_ptr);
     cudaFree(a->col_idx);
     cudaFree(a->values);
+    std::free(a->h_values);
     delete a;
   });
 }

@@ -107,6 +107,23 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// Streaming operands (V, Y, the output) are touched once per step: mark them
+// evict-first in L2 so the 126 MB L2 is left to the gathered W rows, whose
+// stencil reuse distance (one grid plane) is what the cache must cover.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -117,8 +134,11 @@ __device__ __forceinline__ int64_t load_rp(const void* p, int64_t i) {
 }
 
 // ---- the kernel -------------------------------------------------------------------
-template <class F, int G, int CH, int U, int MODE, class RP>
-__global__ void __launch_bounds__(kThreads, 2) cheb_step_kernel(const KArgs p) {
+// G threads per task, CH 16-byte vectors per thread (panel = G*CH vectors), U
+// gathered rows in flight per batch, MINB resident blocks per SM requested from
+// ptxas, HINT = evict-first L2 policy on the streaming operands.
+template <class F, int G, int CH, int U, int MODE, class RP, int MINB, bool HINT>
+__global__ void __launch_bounds__(kThreads, MINB) cheb_step_kernel(const KArgs p) {
   static_assert(kThreads % G == 0 && U <= G && G % U == 0, "bad tiling");
   constexpr int kTasksPerBlock = kThreads / G;
   constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
@@ -138,6 +158,8 @@ __global__ void __launch_bounds__(kThreads, 2) cheb_step_kernel(const KArgs p) {
   const int64_t r = p.row_begin + (task - panel * p.nrows);
   const int64_t cv0 = panel * (G * CH) + lane;  // vector column of chunk 0
   const int64_t rown = r + p.goff;              // own row inside the gathered operand
+  uint64_t pol = 0;
+  if constexpr (HINT) pol = evict_first_policy();
 
   bool cv[CH];
 #pragma unroll
@@ -148,8 +170,15 @@ __global__ void __launch_bounds__(kThreads, 2) cheb_step_kernel(const KArgs p) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       if (cv[c]) {
-        cp_async16(&stage[(2 * c) * kThreads + threadIdx.x], p.vin + r * p.ldv + cv0 + c * G);
-        cp_async16(&stage[(2 * c + 1) * kThreads + threadIdx.x], p.yin + r * p.ldyv + cv0 + c * G);
+        double2* sv = &stage[(2 * c) * kThreads + threadIdx.x];
+        double2* sy = &stage[(2 * c + 1) * kThreads + threadIdx.x];
+        if constexpr (HINT) {
+          cp_async16_hint(sv, p.vin + r * p.ldv + cv0 + c * G, pol);
+          cp_async16_hint(sy, p.yin + r * p.ldyv + cv0 + c * G, pol);
+        } else {
+          cp_async16(sv, p.vin + r * p.ldv + cv0 + c * G);
+          cp_async16(sy, p.yin + r * p.ldyv + cv0 + c * G);
+        }
       }
     }
   }
@@ -228,25 +257,30 @@ __global__ void __launch_bounds__(kThreads, 2) cheb_step_kernel(const KArgs p) {
   for (int c = 0; c < CH; ++c) {
     if (!cv[c]) continue;
     double2* dst = p.out + r * p.ldo + cv0 + c * G;
+    double2 res;
     if constexpr (kStep) {
       // v = (((s0 * aw) + (s1 * w)) - v) + (s2 * y)   (cheb_filter.cpp:170-171, 176-177)
       const double2 vv = stage[(2 * c) * kThreads + threadIdx.x];
       const double2 yy = stage[(2 * c + 1) * kThreads + threadIdx.x];
-      *dst = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own[c])), vv), scale2(p.s2, yy));
+      res = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own[c])), vv), scale2(p.s2, yy));
     } else if constexpr (kFirst) {
       // w = c_d * y ; v = (2 l1) * aw + (2 l2 + c_{d-1}/c_d) * w   (cheb_filter.cpp:162-165)
-      p.wout[r * p.ldo + cv0 + c * G] = own[c];
-      *dst = add2(scale2(p.s0, acc[c]), scale2(p.s1, own[c]));
+      double2* wdst = p.wout + r * p.ldo + cv0 + c * G;
+      if constexpr (HINT) st_hint(wdst, own[c], pol);
+      else *wdst = own[c];
+      res = add2(scale2(p.s0, acc[c]), scale2(p.s1, own[c]));
     } else if constexpr (kDeg1) {
       // c0 * x + c1 * (l1 * ax + l2 * x)   (cheb_filter.cpp:154)
-      *dst = add2(scale2(p.s0, own[c]), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own[c]))));
+      res = add2(scale2(p.s0, own[c]), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own[c]))));
     } else {
-      *dst = acc[c];
+      res = acc[c];
     }
+    if constexpr (HINT) st_hint(dst, res, pol);
+    else *dst = res;
   }
 }
 
-template <class F, int G, int CH, int U, class RP>
+template <class F, int G, int CH, int U, class RP, int MINB, bool HINT>
 void launch_mode(adp_ctx* ctx, StepMode mode, const KArgs& k, int64_t tasks) {
   constexpr int kTasksPerBlock = kThreads / G;
   const int64_t blocks = (tasks + kTasksPerBlock - 1) / kTasksPerBlock;
@@ -254,55 +288,88 @@ void launch_mode(adp_ctx* ctx, StepMode mode, const KArgs& k, int64_t tasks) {
   const dim3 grid(static_cast<unsigned>(blocks));
   switch (mode) {
     case StepMode::First:
-      cheb_step_kernel<F, G, CH, U, 0, RP><<<grid, kThreads, 0, ctx->stream>>>(k);
+      cheb_step_kernel<F, G, CH, U, 0, RP, MINB, HINT><<<grid, kThreads, 0, ctx->stream>>>(k);
       break;
     case StepMode::Step:
-      cheb_step_kernel<F, G, CH, U, 1, RP><<<grid, kThreads, 0, ctx->stream>>>(k);
+      cheb_step_kernel<F, G, CH, U, 1, RP, MINB, HINT><<<grid, kThreads, 0, ctx->stream>>>(k);
       break;
     case StepMode::Deg1:
-      cheb_step_kernel<F, G, CH, U, 2, RP><<<grid, kThreads, 0, ctx->stream>>>(k);
+      cheb_step_kernel<F, G, CH, U, 2, RP, MINB, HINT><<<grid, kThreads, 0, ctx->stream>>>(k);
       break;
     case StepMode::Spmm:
-      cheb_step_kernel<F, G, CH, U, 3, RP><<<grid, kThreads, 0, ctx->stream>>>(k);
+      cheb_step_kernel<F, G, CH, U, 3, RP, MINB, HINT><<<grid, kThreads, 0, ctx->stream>>>(k);
       break;
     case StepMode::SpmmAcc:
-      cheb_step_kernel<F, G, CH, U, 4, RP><<<grid, kThreads, 0, ctx->stream>>>(k);
+      cheb_step_kernel<F, G, CH, U, 4, RP, MINB, HINT><<<grid, kThreads, 0, ctx->stream>>>(k);
       break;
   }
   ADP_LAUNCH_CHECK();
   ctx->launches += 1;
 }
 
+// Panel geometry for a full-warp group: n_panels panels of `ch` 32-vector chunks.
+int64_t panels_for(int64_t qv, int64_t ch) { return (qv + 32 * ch - 1) / (32 * ch); }
+
 template <class F, class RP>
 void dispatch(adp_ctx* ctx, StepMode mode, KArgs k) {
   const int64_t qv = k.qv;
-  // Vectors per panel: up to 4 per lane of a full warp (a 2 KB fp64 row panel),
-  // narrower thread groups for thin blocks so lanes are not idle.
-  int max_vec_panel = 128;
-  if (ctx->panel_cols > 0) {
-    const int epv = std::is_same<F, RealF>::value ? 2 : 1;
-    max_vec_panel = std::max(1, ctx->panel_cols / epv);
-  }
   if (qv <= 4) {
     k.n_panels = 1;
-    launch_mode<F, 4, 1, 4, RP>(ctx, mode, k, k.nrows);
-  } else if (qv <= 8) {
+    launch_mode<F, 4, 1, 4, RP, 2, true>(ctx, mode, k, k.nrows);
+    return;
+  }
+  if (qv <= 8) {
     k.n_panels = 1;
-    launch_mode<F, 8, 1, 8, RP>(ctx, mode, k, k.nrows);
-  } else if (qv <= 16) {
+    launch_mode<F, 8, 1, 8, RP, 2, true>(ctx, mode, k, k.nrows);
+    return;
+  }
+  if (qv <= 16) {
     k.n_panels = 1;
-    launch_mode<F, 16, 1, 8, RP>(ctx, mode, k, k.nrows);
-  } else {
-    const int64_t per_panel_cap = std::max<int64_t>(32, std::min<int64_t>(128, max_vec_panel));
-    const int64_t n_panels = (qv + per_panel_cap - 1) / per_panel_cap;
-    const int64_t ch = (((qv + n_panels - 1) / n_panels) + 31) / 32;  // chunks of 32 vectors
-    k.n_panels = (qv + 32 * ch - 1) / (32 * ch);
-    const int64_t tasks = k.nrows * k.n_panels;
-    switch (ch) {
-      case 1: launch_mode<F, 32, 1, 8, RP>(ctx, mode, k, tasks); break;
-      case 2: launch_mode<F, 32, 2, 4, RP>(ctx, mode, k, tasks); break;
-      case 3: launch_mode<F, 32, 3, 4, RP>(ctx, mode, k, tasks); break;
-      default: launch_mode<F, 32, 4, 4, RP>(ctx, mode, k, tasks); break;
+    launch_mode<F, 16, 1, 8, RP, 2, true>(ctx, mode, k, k.nrows);
+    return;
+  }
+  // Tuning variants (adp_ctx_set_tuning); 0 = default.
+  int variant = ctx->variant;
+  if (ctx->panel_cols > 0) {  // explicit panel width: closest chunk count
+    const int epv = std::is_same<F, RealF>::value ? 2 : 1;
+    const int64_t ch = std::max<int64_t>(1, std::min<int64_t>(4, ctx->panel_cols / epv / 32));
+    variant = ch == 1 ? 4 : (ch == 2 ? 2 : 1);
+  }
+  auto go = [&](int64_t ch, auto launcher) {
+    k.n_panels = panels_for(qv, ch);
+    launcher(k.nrows * k.n_panels);
+  };
+  switch (variant) {
+    case 1:  // 4 chunks (2 KB fp64 panels), evict-first streaming
+      go(4, [&](int64_t t) { launch_mode<F, 32, 4, 4, RP, 2, true>(ctx, mode, k, t); });
+      break;
+    case 2:  // 2 chunks (1 KB panels), 3 blocks / SM
+      go(2, [&](int64_t t) { launch_mode<F, 32, 2, 4, RP, 3, true>(ctx, mode, k, t); });
+      break;
+    case 3:  // 2 chunks, 8 rows in flight
+      go(2, [&](int64_t t) { launch_mode<F, 32, 2, 8, RP, 2, true>(ctx, mode, k, t); });
+      break;
+    case 4:  // 1 chunk (512 B panels), 3 blocks / SM
+      go(1, [&](int64_t t) { launch_mode<F, 32, 1, 8, RP, 3, true>(ctx, mode, k, t); });
+      break;
+    case 5:  // 1 chunk, 4 blocks / SM
+      go(1, [&](int64_t t) { launch_mode<F, 32, 1, 8, RP, 4, true>(ctx, mode, k, t); });
+      break;
+    case 6:  // 2 chunks, 4 blocks / SM
+      go(2, [&](int64_t t) { launch_mode<F, 32, 2, 4, RP, 4, true>(ctx, mode, k, t); });
+      break;
+    case 7:  // 4 chunks, no cache hints (round-1 baseline)
+      go(4, [&](int64_t t) { launch_mode<F, 32, 4, 4, RP, 2, false>(ctx, mode, k, t); });
+      break;
+    default: {  // automatic: <= 4 chunks per panel, balanced across panels
+      const int64_t n_panels = (qv + 127) / 128;
+      const int64_t ch = (((qv + n_panels - 1) / n_panels) + 31) / 32;
+      switch (ch) {
+        case 1: go(1, [&](int64_t t) { launch_mode<F, 32, 1, 8, RP, 3, true>(ctx, mode, k, t); }); break;
+        case 2: go(2, [&](int64_t t) { launch_mode<F, 32, 2, 4, RP, 3, true>(ctx, mode, k, t); }); break;
+        case 3: go(3, [&](int64_t t) { launch_mode<F, 32, 3, 4, RP, 2, true>(ctx, mode, k, t); }); break;
+        default: go(4, [&](int64_t t) { launch_mode<F, 32, 4, 4, RP, 2, true>(ctx, mode, k, t); }); break;
+      }
     }
   }
 }
@@ -313,12 +380,18 @@ void launch_step(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
   const bool cplx = a->dtype == ADP_C128;
   const int epv = cplx ? 1 : 2;
-  if (s.ld % epv || s.ld_out % epv || s.ld_y % epv) fail(ADP_ERR_DIMENSION, "cheb_step: leading dimension must be even for fp64");
+  if (s.ld % epv || s.ld_out % epv || s.ld_y % epv)
+    fail(ADP_ERR_DIMENSION, "cheb_step: leading dimension must be even for fp64");
   auto aligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
   if (!aligned(s.gsrc) || !aligned(s.out) || (s.vin && !aligned(s.vin)) || (s.yin && !aligned(s.yin)) ||
       (s.wout && !aligned(s.wout)))
     fail(ADP_ERR_DIMENSION, "cheb_step: operands must be 16-byte aligned");
   if (s.row_end <= s.row_begin || s.q == 0) return;
+  // B200 path: the TMA-pipelined tile kernel (cheb_tile.cu). Variants 1-7 force
+  // the row kernel below (tuning comparisons); it also serves thin blocks and
+  // operators whose rows do not fit a shared-memory stage.
+  if (ctx->tile_ch > 0 && launch_step_tiled(ctx, mode, s)) return;
+  if ((ctx->variant == 0 || ctx->variant > 10) && launch_step_row(ctx, mode, s)) return;
   KArgs k{};
   k.row_ptr = a->row_ptr;
   k.col = a->col_idx;

@@ -42,8 +42,12 @@ class Context:
             pass
 
     def set_stream(self, stream) -> None:
-        """Queue work on an existing cudaStream_t (int handle or torch.cuda.Stream); None = own stream."""
-        handle = 0 if stream is None else int(getattr(stream, "cuda_stream", stream))
+        """Queue work on an existing cudaStream_t (int handle or torch.cuda.Stream; 0 = legacy default
+        stream, torch's default). None = the context's own non-blocking stream."""
+        if stream is None:
+            handle = lib().adp_ctx_own_stream(self.h) or 0
+        else:
+            handle = int(getattr(stream, "cuda_stream", stream))
         check(lib().adp_ctx_set_stream(self.h, C.c_void_p(handle)))
 
     def synchronize(self) -> None:
@@ -55,6 +59,12 @@ class Context:
 
     def set_panel(self, cols: int) -> None:
         check(lib().adp_ctx_set_panel(self.h, int(cols)))
+
+    def set_tuning(self, variant: int) -> None:
+        check(lib().adp_ctx_set_tuning(self.h, int(variant)))
+
+    def set_tile_config(self, chunks: int = 0, stages: int = 0, stage_kib: int = 0, ctas_per_sm: int = 0) -> None:
+        check(lib().adp_ctx_set_tile_config(self.h, int(chunks), int(stages), int(stage_kib), int(ctas_per_sm)))
 
 
 _default_ctx: dict[int, Context] = {}

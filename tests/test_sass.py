@@ -1,0 +1,68 @@
+"""SASS-level checks of libadp_b200.so (CPU only: cuobjdump, no GPU).
+
+* every kernel is compiled for sm_100a;
+* the TMA tile kernel really issues bulk copies (UBLKCP) and the row kernels
+  LDGSTS (cp.async);
+* no global access uses an odd-numbered uniform descriptor register: ptxas
+  12.9 produced such code for cache-hinted cp.async in one kernel shape, and
+  it faults at run time (illegal instruction) -- this guards the workaround;
+* the fused step kernels contain no FMA (DFMA): the bitwise-parity contract
+  relies on unfused multiplies and adds.
+"""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_2604_00914_b200", "libadp_b200.so")
+
+
+@pytest.fixture(scope="module")
+def sass():
+    if not shutil.which("cuobjdump") and not os.path.exists("/usr/local/cuda/bin/cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([exe, "-sass", LIB], capture_output=True, text=True, check=True).stdout
+    funcs = {}
+    cur = None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur and re.match(r"\s+/\*[0-9a-f]+\*/", line):
+            funcs[cur].append(line)
+    return out, funcs
+
+
+def test_arch_is_sm100a(sass):
+    out, funcs = sass
+    assert "arch = sm_100a" in out
+    assert len(funcs) > 50
+
+
+def test_tma_and_async_copies_present(sass):
+    _, funcs = sass
+    tile = [f for f in funcs if "cheb_tile_kernel" in f]
+    assert tile and all(any("UBLKCP" in ln for ln in funcs[f]) for f in tile if "ELi1EEEv" in f)
+    lean_step = [f for f in funcs if "cheb_lean_kernel" in f and re.search(r"ELi1E[il]Li\dELb", f)]
+    assert lean_step and all(any("LDGSTS" in ln for ln in funcs[f]) for f in lean_step)
+
+
+def test_no_odd_uniform_descriptors(sass):
+    _, funcs = sass
+    bad = [f for f, lines in funcs.items()
+           if any(re.search(r"desc\[UR([0-9]+)\]", ln) and int(re.search(r"desc\[UR([0-9]+)\]", ln).group(1)) % 2
+                  for ln in lines)]
+    assert not bad, bad[:3]
+
+
+def test_step_kernels_have_no_fma(sass):
+    _, funcs = sass
+    step = [f for f in funcs if re.search(r"cheb_(step|row|lean|tile)_kernel", f)]
+    assert step
+    fused = [f for f in step if any(re.search(r"\bDFMA\b", ln) for ln in funcs[f])]
+    assert not fused, fused[:3]

@@ -1,0 +1,45 @@
+"""Summarise an ncu report (raw page) into the metrics the roofline needs. Usage: ncu_summary.py rep [rep...]"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum", "lts__t_sector_hit_rate.pct",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__t_sector_hit_rate.pct",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__inst_executed.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
+
+
+def summary(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for vals in rows[2:]:
+        d = {}
+        for i, h in enumerate(hdr):
+            if h in KEYS:
+                d[h] = (vals[i], units[i])
+        stalls = []
+        for i, h in enumerate(hdr):
+            if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
+                try:
+                    stalls.append((float(vals[i].replace(",", "")), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+                except ValueError:
+                    pass
+        stalls.sort(reverse=True)
+        d["top_stalls"] = stalls[:6]
+        res.append(d)
+    return res
+
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        for d in summary(p):
+            print(f"== {p}")
+            for k in KEYS:
+                if k in d:
+                    print(f"  {k}: {d[k][0]} {d[k][1]}")
+            print("  stalls:", ", ".join(f"{n}={int(v)}" for v, n in d["top_stalls"]))

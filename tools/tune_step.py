@@ -1,0 +1,69 @@
+"""Sweep the fused-step kernel's tuning variants on one configuration (GPU).
+
+Prints ms per degree-step launch and effective GB/s for each variant, and
+checks that every variant's result is bitwise identical to variant 0's.
+Usage: python tools/tune_step.py [--config c2] [--degree 30] [--variants 0,1,2]
+"""
+import argparse
+import math
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_2604_00914_b200 as adp  # noqa: E402
+from paper_2604_00914_b200 import configs  # noqa: E402
+import bench  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", default="c2")
+    p.add_argument("--degree", type=int, default=30)
+    p.add_argument("--variants", default="1", help="row-kernel variants (1-7); 0 = automatic")
+    p.add_argument("--tiles", default="", help="tile configs 'ch,stages,kib,ctas;...' (0 = default)")
+    p.add_argument("--reps", type=int, default=3)
+    args = p.parse_args()
+    cfg = configs.CONFIGS[args.config]
+    a = cfg.operator()
+    n, nnz, q = a.n_rows, a.nnz, cfg.q
+    k1 = configs.filter_degree(cfg)
+    f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, max(args.degree, int(math.ceil(2.5 * k1))), 0.5)
+    ctx = adp.Context(0)
+    ctx.set_stream(torch.cuda.current_stream())
+    da = adp.DeviceCsr(a, ctx)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    dt = torch.complex128 if a.is_complex else torch.float64
+    x = torch.randn(n, q, dtype=dt, device="cuda", generator=g)
+    ref = None
+    b_step = bench.step_bytes(n, nnz, q, s=16 if a.is_complex else 8)
+    runs = [("row", int(s), None) for s in args.variants.split(",") if s]
+    for spec in filter(None, args.tiles.split(";")):
+        runs.append(("tile", 0, [int(x) for x in spec.split(",")]))
+    for kind, v, tcfg in runs:
+        ctx.set_tuning(v)
+        ctx.set_tile_config(*(tcfg or [0, 0, 0, 0]))
+        y = torch.empty_like(x)
+        adp.clenshaw_apply_device(f, da, x, args.degree, out=y)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.reps):
+            adp.clenshaw_apply_device(f, da, x, args.degree, out=y)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.reps / args.degree
+        same = None
+        if ref is None:
+            ref = y.clone()
+        else:
+            same = bool(torch.equal(ref, y))
+        label = f"variant {v}" if kind == "row" else f"tile ch,stages,kib,ctas={tcfg}"
+        print(f"{args.config} q={q} {label}: {ms:.4f} ms/launch  {b_step / ms / 1e6:.1f} GB/s  "
+              f"bitwise_vs_first={same}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
