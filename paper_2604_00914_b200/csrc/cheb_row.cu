@@ -102,6 +102,42 @@ __device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, ui
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol)
                : "memory");
 }
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -397,19 +433,26 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const RArgs p
   const char* gb = reinterpret_cast<const char*>(p.g) + voff;
   const uint64_t pol = policy_evict_first_rt(p.pol_frac);
 
-  double2* my = ring + warp * (2 * CH * 32);
+  // V[r], Y[r] panels arrive by TMA bulk copies (lane 0, L2 evict-first hint)
+  // into this warp's shared-memory slot, completing on the warp's mbarrier.
+  // The epilogue operands V[r], Y[r] arrive by TMA bulk copies (lane 0, L2
+  // evict-first hint) into this warp's shared-memory slot, completing on the
+  // warp's mbarrier. (The own W row stays an L1-hit __ldg: staging it too
+  // grew the carve-out and cost more in L1 hits than it saved -- measured.)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ring) + warp;
+  double2* my = ring + 8 + warp * (2 * CH * 32);  // 8 x 16 B header holds the 8 mbarriers
+  constexpr uint32_t kPB = 32u * CH * 16u;
   if constexpr (kStep) {
-    const char* vsrc = reinterpret_cast<const char*>(p.vin) + static_cast<uint64_t>(r) * ldg_b + voff;
-    const char* ysrc = reinterpret_cast<const char*>(p.yin) + static_cast<uint64_t>(r) * (static_cast<uint32_t>(p.ldyv) * 16u) + voff;
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      // No L2 cache-hint on these copies: with the hint, ptxas 12.9 emits
-      // LDGSTS with an odd-numbered descriptor register here, which faults at
-      // run time (illegal instruction); tests/test_sass.py guards against it.
-      cp_async16(&my[(0 * CH + c) * 32 + lane], vsrc + 512 * c);
-      cp_async16(&my[(1 * CH + c) * 32 + lane], ysrc + 512 * c);
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
+      const char* vsrc = reinterpret_cast<const char*>(p.vin) + static_cast<uint64_t>(r) * ldg_b + poff;
+      const char* ysrc = reinterpret_cast<const char*>(p.yin) + static_cast<uint64_t>(r) * (static_cast<uint32_t>(p.ldyv) * 16u) + poff;
+      mbar_arrive_expect_tx(bar, 2 * kPB);
+      bulk_g2s_hint(my, vsrc, kPB, bar, pol);
+      bulk_g2s_hint(my + CH * 32, ysrc, kPB, bar, pol);
     }
-    cp_async_commit();
   }
   const char* ob = reinterpret_cast<char*>(p.out) + static_cast<uint64_t>(r) * (static_cast<uint32_t>(p.ldo) * 16u) + voff;
 
@@ -454,7 +497,10 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const RArgs p
       }
     }
   }
-  if constexpr (kStep) cp_async_wait<0>();
+  if constexpr (kStep) {
+    __syncwarp();
+    mbar_wait(bar, 0);
+  }
   const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * ldg_b);
   char* wb = kFirst ? reinterpret_cast<char*>(p.wout) + static_cast<uint64_t>(r) * (static_cast<uint32_t>(p.ldo) * 16u) + voff : nullptr;
 #pragma unroll
@@ -487,7 +533,7 @@ void launch_lean(adp_ctx* ctx, StepMode mode, RArgs k) {
   const int64_t total = k.nrows * k.n_panels;
   if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_lean: too many tasks");
   const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
-  const size_t smem = mode == StepMode::Step ? static_cast<size_t>(kWarps) * 2 * CH * 32 * 16 : 16;
+  const size_t smem = mode == StepMode::Step ? 128 + static_cast<size_t>(kWarps) * 2 * CH * 32 * 16 : 16;
   auto run = [&](auto kern) {
     if (smem > 48 * 1024)
       ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -517,22 +563,21 @@ void launch_lean(adp_ctx* ctx, StepMode mode, RArgs k) {
 
 template <class F, class RP>
 void dispatch_row(adp_ctx* ctx, StepMode mode, const RArgs& k, int pipe_variant) {
+  // tuning variants (adp_ctx_set_tuning 11..15): lean kernel geometry (CH, U, MINB)
   switch (pipe_variant) {
-    case 1: launch_ch<F, RP, 4, 4, 2>(ctx, mode, k); return;
-    case 2: launch_ch<F, RP, 2, 8, 2>(ctx, mode, k); return;
-    case 3: launch_ch<F, RP, 2, 4, 3>(ctx, mode, k); return;
-    case 4:
-      if (k.qv % 128 == 0) { launch_lean<F, 4, 4, RP, 2>(ctx, mode, k); return; }
-      break;
-    case 5:
-      if (k.qv % 64 == 0) { launch_lean<F, 2, 8, RP, 2>(ctx, mode, k); return; }
-      break;
+    case 1: if (k.qv % 32 == 0) { launch_lean<F, 1, 1, RP, 8>(ctx, mode, k); return; } break;
+    case 2: if (k.qv % 32 == 0) { launch_lean<F, 1, 4, RP, 6>(ctx, mode, k); return; } break;
+    case 3: if (k.qv % 64 == 0) { launch_lean<F, 2, 1, RP, 6>(ctx, mode, k); return; } break;
+    case 4: if (k.qv % 128 == 0) { launch_lean<F, 4, 4, RP, 2>(ctx, mode, k); return; } break;
+    case 5: if (k.qv % 64 == 0) { launch_lean<F, 2, 2, RP, 5>(ctx, mode, k); return; } break;
     default: break;
   }
   // automatic: lean kernel on full panels (widest of 4 / 2 / 1 vectors per lane), else pipelined
-  if (k.qv % 128 == 0) return launch_lean<F, 4, 4, RP, 2>(ctx, mode, k);
-  if (k.qv % 64 == 0) return launch_lean<F, 2, 8, RP, 2>(ctx, mode, k);
-  if (k.qv % 32 == 0) return launch_lean<F, 1, 8, RP, 3>(ctx, mode, k);
+  // (measured on config 2: one gathered row in flight per warp and more resident
+  //  warps beats deeper per-warp batches -- CH 4, U 1, 4 blocks/SM: 83% of HBM)
+  if (k.qv % 128 == 0) return launch_lean<F, 4, 1, RP, 4>(ctx, mode, k);
+  if (k.qv % 64 == 0) return launch_lean<F, 2, 1, RP, 6>(ctx, mode, k);
+  if (k.qv % 32 == 0) return launch_lean<F, 1, 1, RP, 8>(ctx, mode, k);
   const int64_t n4 = (k.qv + 127) / 128;
   const int64_t ch = ((k.qv + n4 - 1) / n4 + 31) / 32;
   if (ch >= 4) launch_ch<F, RP, 4, 4, 2>(ctx, mode, k);

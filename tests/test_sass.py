@@ -49,7 +49,9 @@ def test_tma_and_async_copies_present(sass):
     tile = [f for f in funcs if "cheb_tile_kernel" in f]
     assert tile and all(any("UBLKCP" in ln for ln in funcs[f]) for f in tile if "ELi1EEEv" in f)
     lean_step = [f for f in funcs if "cheb_lean_kernel" in f and re.search(r"ELi1E[il]Li\dELb", f)]
-    assert lean_step and all(any("LDGSTS" in ln for ln in funcs[f]) for f in lean_step)
+    assert lean_step and all(any("UBLKCP" in ln for ln in funcs[f]) for f in lean_step)
+    row_step = [f for f in funcs if "cheb_row_kernel" in f and re.search(r"ELi1E[il]Li\dELb", f)]
+    assert row_step and all(any("LDGSTS" in ln for ln in funcs[f]) for f in row_step)
 
 
 def test_no_odd_uniform_descriptors(sass):
