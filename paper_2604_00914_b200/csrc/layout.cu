@@ -95,10 +95,12 @@ __device__ __forceinline__ uint4 philox_block(uint64_t seed, uint64_t stream, ui
 __global__ void fill_philox_kernel(double* dst, int64_t n, int64_t q, int64_t ld, uint64_t seed, uint64_t stream,
                                    int kind) {
   const int64_t total = n * q;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t c = i / n, r = i - c * n;
-    const uint64_t idx = static_cast<uint64_t>(i);
+  // walk the storage (row-major) order so the writes coalesce; the draw index
+  // is still the reference's column-major c*n + r
+  for (int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < total;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = s / q, c = s - r * q;
+    const uint64_t idx = static_cast<uint64_t>(c * n + r);
     const uint4 b = philox_block(seed, stream, idx / 4);
     const uint32_t w[4] = {b.x, b.y, b.z, b.w};
     double v;
