@@ -152,6 +152,74 @@ adp_status adp_fill_gaussian_device(adp_ctx* ctx, double* d_out, int64_t n, int6
 adp_status adp_fill_rademacher_device(adp_ctx* ctx, double* d_out, int64_t n, int64_t q, int64_t ld,
                                       uint64_t seed, uint64_t stream);
 
+/* ------------------------------------------------- device solver subsystems -- */
+/* estimate_spectrum_bounds (include/adapoly/lanczos.hpp:24-26, src/lanczos.cpp:81-111):
+ * 40-step Lanczos with full reorthogonalisation on the device. */
+adp_status adp_lanczos_bounds(adp_ctx* ctx, const adp_csr* a, int32_t steps, uint64_t seed, double* lambda_min,
+                              double* lambda_max, int64_t* spmv_count);
+/* estimate_eigcount (include/adapoly/solver.hpp:102-103, src/solver.cpp:108-117). */
+adp_status adp_estimate_eigcount(adp_ctx* ctx, const adp_csr* a, const double* coeffs, int32_t k_max, double l1,
+                                 double l2, int64_t probes, uint64_t seed, double* out, int64_t* spmv_count);
+/* cholesky_qr (include/adapoly/dense_kernels.hpp:22, src/dense_kernels.cpp:53-92) in place on a
+ * device row-major n x p block; *kept = orthonormal columns (dependent ones dropped, compacted). */
+adp_status adp_cholesky_qr_device(adp_ctx* ctx, double* x, int64_t n, int64_t p, int64_t ld, int64_t* kept);
+/* rayleigh_ritz (include/adapoly/dense_kernels.hpp:31, src/dense_kernels.cpp:94-101): theta
+ * (host, ascending, qc doubles), V = Q U written to v_out (device row-major, ldv). */
+adp_status adp_rayleigh_ritz_device(adp_ctx* ctx, const adp_csr* a, const double* q, int64_t ld, int64_t qc,
+                                    double* theta, double* v_out, int64_t ldv);
+/* compute_residuals (include/adapoly/solver.hpp:96-98, src/solver.cpp:94-106): norms (host). */
+adp_status adp_residual_norms_device(adp_ctx* ctx, const adp_csr* a, const double* v, int64_t ld, int64_t e,
+                                     const double* lambda, double* norms);
+/* spurious_threshold (include/adapoly/solver.hpp:92, src/solver.cpp:81-92). */
+adp_status adp_spurious_threshold(const double* ritz, int64_t n, double a, double b, double* out);
+
+/* ------------------------------------------------------------------ solve -- */
+/* SolverConfig (include/adapoly/solver.hpp:14-32); p_override <= 0 means "none".
+ * tile_ti / tile_tk have no meaning on the device and are omitted. */
+typedef struct {
+  double interval_a, interval_b;
+  double tau_c, tau_a, m, c, k_multiplier, mu;
+  int64_t max_iter, lanczos_steps, trace_probes;
+  uint64_t rng_seed;
+  int64_t p_override;
+  int32_t spurious_detection, collect_diagnostics;
+} adp_solver_config;
+
+/* IterationRecord (include/adapoly/solver.hpp:49-59). */
+typedef struct {
+  int64_t iteration;
+  int32_t degree;
+  int64_t active_width, e_in_interval, n_locked_total;
+  double max_residual;
+  int64_t spmv_filter, spmv_residual;
+  double orth_error;
+} adp_iteration_record;
+
+/* StageTimings (include/adapoly/solver.hpp:61-68), seconds. */
+typedef struct {
+  double setup, filter, orth, rayleigh_ritz, residuals, other;
+} adp_stage_timings;
+
+/* SolveResult scalars (include/adapoly/solver.hpp:70-85). */
+typedef struct {
+  int64_t n, n_eigs, iterations, spmv_total, subspace_dim, n_history;
+  int32_t converged, dense_fallback;
+  double avg_degree, max_residual, e_estimate, lambda_min, lambda_max;
+  adp_stage_timings timings;
+} adp_solve_summary;
+
+typedef struct adp_solve_result adp_solve_result;
+
+void adp_solver_config_default(adp_solver_config* cfg);
+/* solve (include/adapoly/solver.hpp:106, src/solver.cpp:119-360) on a real symmetric operator. */
+adp_status adp_solve(adp_ctx* ctx, const adp_csr* a, const adp_solver_config* cfg, adp_solve_result** out);
+adp_status adp_solve_summary_get(const adp_solve_result* r, adp_solve_summary* s);
+/* eigenvalues ascending (n_eigs doubles); eigenvectors column-major n x n_eigs with ldv (either may be NULL). */
+adp_status adp_solve_eigenpairs(const adp_solve_result* r, double* values, double* vectors, int64_t ldv);
+/* n_history records and degrees (either may be NULL). */
+adp_status adp_solve_history(const adp_solve_result* r, adp_iteration_record* records, int32_t* degree_history);
+adp_status adp_solve_result_destroy(adp_solve_result* r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -414,6 +414,10 @@ double orc_mt_uniform(void* h, double lo, double hi) {
     std::uniform_real_distribution<double> u(lo, hi);
     return u(*static_cast<std::mt19937_64*>(h));
 }
+std::int64_t orc_mt_uniform_int(void* h, std::int64_t lo, std::int64_t hi) {
+    std::uniform_int_distribution<std::int64_t> u(lo, hi);
+    return u(*static_cast<std::mt19937_64*>(h));
+}
 int orc_mt_bernoulli(void* h, double p) {
     std::bernoulli_distribution b(p);
     return b(*static_cast<std::mt19937_64*>(h)) ? 1 : 0;

@@ -81,6 +81,7 @@ def lib():
             "orc_mt_next": (U64, [P]),
             "orc_mt_uniform": (D, [P, D, D]),
             "orc_mt_bernoulli": (I, [P, D]),
+            "orc_mt_uniform_int": (I64, [P, I64, I64]),
             "orc_csr_from_triplets": (I, [I64, I64, I64, P, P, P, P]),
             "orc_random_csr": (P, [I64, I64, D, U64]),
             "orc_random_symmetric": (P, [I64, D, U64]),
@@ -197,6 +198,9 @@ class MT19937_64:
 
     def bernoulli(self, p: float = 0.5) -> bool:
         return bool(lib().orc_mt_bernoulli(self.h, p))
+
+    def uniform_int(self, lo: int, hi: int) -> int:
+        return lib().orc_mt_uniform_int(self.h, lo, hi)
 
 
 # --------------------------------------------------------------------- CSR ---

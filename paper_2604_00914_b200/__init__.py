@@ -10,6 +10,9 @@ from .filter import (ChebFilter, SpectrumBounds, adaptive_degree, build_filter, 
                      eval_filter_scalar, initial_degree, jackson_damping, lanczos_damping)
 from .operator import (Context, DeviceCsr, clenshaw_apply, clenshaw_apply_device, default_context, maspmm,
                        maspmm_device)
+from .solver import (IterationRecord, SolveResult, SolverConfig, StageTimings, cholesky_qr_device,
+                     compute_residuals_device, estimate_eigcount, estimate_spectrum_bounds, rayleigh_ritz_device,
+                     solve, spurious_threshold)
 from .sparse import (CsrMatrix, fill_gaussian, fill_rademacher, parse_matrix_market, philox_block,
                      philox_gaussian, philox_uniform, read_matrix_market)
 
@@ -19,5 +22,7 @@ __all__ = [
     "chebyshev_step_coeffs", "eval_filter_scalar", "initial_degree", "jackson_damping", "lanczos_damping",
     "Context", "DeviceCsr", "clenshaw_apply", "clenshaw_apply_device", "default_context", "maspmm",
     "maspmm_device", "CsrMatrix", "fill_gaussian", "fill_rademacher", "parse_matrix_market", "philox_block",
-    "philox_gaussian", "philox_uniform", "read_matrix_market",
+    "philox_gaussian", "philox_uniform", "read_matrix_market", "IterationRecord", "SolveResult", "SolverConfig",
+    "StageTimings", "cholesky_qr_device", "compute_residuals_device", "estimate_eigcount",
+    "estimate_spectrum_bounds", "rayleigh_ritz_device", "solve", "spurious_threshold",
 ]

@@ -103,6 +103,18 @@ SIGNATURES = {
     "adp_philox_block": (I32, [U64, U64, U64, P]),
     "adp_fill_gaussian_device": (I32, [P, P, I64, I64, I64, U64, U64]),
     "adp_fill_rademacher_device": (I32, [P, P, I64, I64, I64, U64, U64]),
+    "adp_lanczos_bounds": (I32, [P, P, I32, U64, P, P, P]),
+    "adp_estimate_eigcount": (I32, [P, P, P, I32, D, D, I64, U64, P, P]),
+    "adp_cholesky_qr_device": (I32, [P, P, I64, I64, I64, P]),
+    "adp_rayleigh_ritz_device": (I32, [P, P, P, I64, I64, P, P, I64]),
+    "adp_residual_norms_device": (I32, [P, P, P, I64, I64, P, P]),
+    "adp_spurious_threshold": (I32, [P, I64, D, D, P]),
+    "adp_solver_config_default": (None, [P]),
+    "adp_solve": (I32, [P, P, P, P]),
+    "adp_solve_summary_get": (I32, [P, P]),
+    "adp_solve_eigenpairs": (I32, [P, P, P, I64]),
+    "adp_solve_history": (I32, [P, P, P]),
+    "adp_solve_result_destroy": (I32, [P]),
 }
 
 _lib = None

@@ -193,7 +193,7 @@ adp_status adp_ctx_create(int32_t device, adp_ctx** out) {
   });
 }
 
-void adp_release_dense_handles(adp_ctx* ctx);  // dense.cu
+void adp_release_dense_handles(adp_ctx* ctx);  // dense.cu (extern "C")
 
 adp_status adp_ctx_destroy(adp_ctx* ctx) {
   return guarded([&] {

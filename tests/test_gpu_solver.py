@@ -1,0 +1,326 @@
+"""Device solver subsystems and solve(), restating the reference's own tests.
+
+proj/tests/test_eigensolver.cpp (all 22 cases) and proj/tests/test_dense_kernels.cpp
+(CholQR2 / Rayleigh-Ritz properties) against the GPU path, on the reference's
+own generators (oracle: libstdc++ mt19937_64 + distributions, bit for bit). The
+dense eigenvalue oracle is numpy.linalg.eigvalsh (the reference uses Eigen's
+SelfAdjointEigenSolver: tests/support/test_matrices.hpp:78-81). Tolerances are
+the reference's.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2604_00914_b200 as adp
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = adp.Context(0)
+    yield c
+    c.close()
+
+
+def dev(ctx, a):
+    return adp.DeviceCsr(adp.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values), ctx)
+
+
+def iota_diag(orc, n):
+    return orc.make_diag(np.arange(1, n + 1, dtype=np.float64))
+
+
+def spectrum(a):
+    return np.linalg.eigvalsh(a.to_dense())
+
+
+# ------------------------------------------------------ estimate_spectrum_bounds ---
+def test_bounds_exact_at_full_krylov(ctx, orc):  # test_eigensolver.cpp:28-37
+    a = dev(ctx, iota_diag(orc, 10))
+    b = adp.estimate_spectrum_bounds(a, 10, 3)
+    assert b.lambda_min <= 1.0 and b.lambda_max >= 10.0
+    assert b.lambda_min >= 1.0 - 1e-8 and b.lambda_max <= 10.0 + 1e-8
+    with pytest.raises(adp.ConfigError):
+        adp.estimate_spectrum_bounds(a, 1, 3)
+
+
+def test_bounds_identity_widened(ctx, orc):  # :39-45
+    b = adp.estimate_spectrum_bounds(dev(ctx, orc.make_diag(np.ones(50))), 10, 1)
+    assert b.lambda_min < 1.0 < b.lambda_max and b.lambda_max - b.lambda_min >= 1e-8
+
+
+def test_bounds_deterministic(ctx, orc):  # :47-57
+    a = dev(ctx, orc.random_symmetric(80, 0.1, 5))
+    s1, s2 = [0], [0]
+    b1 = adp.estimate_spectrum_bounds(a, 25, 42, s1)
+    b2 = adp.estimate_spectrum_bounds(a, 25, 42, s2)
+    assert b1 == b2 and s1[0] == s2[0] and s1[0] >= 25
+
+
+def test_bounds_enclose_oracle_extremes(ctx, orc):  # :59-70
+    m = orc.random_symmetric(300, 0.05, 77)
+    sp = spectrum(m)
+    a = dev(ctx, m)
+    enclosed = sum(1 for seed in range(100)
+                   if (lambda b: b.lambda_min <= sp[0] and b.lambda_max >= sp[-1])(
+                       adp.estimate_spectrum_bounds(a, 40, seed)))
+    assert enclosed >= 99
+
+
+# ------------------------------------------------------------- estimate_eigcount ---
+def test_eigcount_sharp_filter(ctx, orc):  # :72-93
+    rng = orc.MT19937_64(13)
+    d = [rng.uniform(-1.0, 0.0) for _ in range(100)]
+    for i, v in ((3, 0.45), (17, 0.5), (42, 0.55), (66, 0.41), (90, 0.59)):
+        d[i] = v
+    a = dev(ctx, orc.make_diag(d))
+    f = adp.build_filter(0.4, 0.6, (-1.05, 1.05), 400, 0.5)
+    for seed in range(5):
+        e = adp.estimate_eigcount(a, f, 40, seed)
+        assert 4.0 <= e <= 6.0
+    with pytest.raises(adp.ConfigError):
+        adp.estimate_eigcount(a, f, 0, 1)
+
+
+def test_eigcount_full_interval_exact(ctx, orc):  # :95-103
+    a = dev(ctx, orc.random_symmetric(64, 0.1, 21))
+    f = adp.build_filter(-50.0, 50.0, (-50.0, 50.0), 30, 0.5)
+    spmv = [0]
+    assert adp.estimate_eigcount(a, f, 7, 9, spmv) == 64.0 and spmv[0] == 0
+
+
+def test_eigcount_matches_oracle(ctx, orc):
+    # same probes, same filter; only the dot-product association order differs from the CPU oracle
+    m = orc.random_symmetric(200, 0.05, 3)
+    sp = spectrum(m)
+    bounds = (sp[0] - 0.1, sp[-1] + 0.1)
+    f = adp.build_filter(sp[60], sp[90], bounds, 120, 0.5)
+    g = orc.build_filter(sp[60], sp[90], bounds, 120, 0.5)
+    got = adp.estimate_eigcount(dev(ctx, m), f, 30, 4)
+    want = orc.estimate_eigcount(orc.Tiled(m, 256, 64), g, 30, 4)
+    assert abs(got - want) <= 1e-10 * max(1.0, abs(want))
+
+
+# ------------------------------------------------------------------ thresholds ---
+def test_spurious_threshold():  # :105-118
+    assert adp.spurious_threshold([0.2, 0.9], 0.0, 1.0) == pytest.approx(0.1)
+    assert adp.spurious_threshold([0.5], 0.0, 1.0) == pytest.approx(0.5)
+    assert adp.spurious_threshold([0.0, 0.4], 0.0, 1.0) == 0.0
+    with pytest.raises(adp.ConfigError):
+        adp.spurious_threshold([], 0.0, 1.0)
+    with pytest.raises(adp.ConfigError):
+        adp.spurious_threshold([1.5], 0.0, 1.0)
+
+
+# ------------------------------------------------------------ compute_residuals ---
+def tcuda(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def test_residuals_exact_eigenpair(ctx, orc):  # :120-133
+    a = dev(ctx, iota_diag(orc, 20))
+    v = np.zeros((20, 2))
+    v[4, 0] = 1.0
+    v[11, 1] = 1.0
+    r = adp.compute_residuals_device(a, tcuda(v), [5.0, 12.0])
+    assert r[0] <= 1e-14 * 20 and r[1] <= 1e-14 * 20
+
+
+def test_residuals_pythagorean(ctx, orc):  # :135-146
+    m = orc.random_symmetric(40, 0.2, 33)
+    v = orc.fill_gaussian(40, 1, 6, 0)[:, 0]
+    v = v / np.linalg.norm(v)
+    av = orc.csr_spmv(m, v)
+    lam = float(v @ av)
+    r = adp.compute_residuals_device(dev(ctx, m), tcuda(v[:, None].copy()), [lam])
+    assert r[0] ** 2 == pytest.approx(float(av @ av) - lam * lam, rel=1e-12)
+
+
+def test_residuals_first_order(ctx, orc):  # :148-166
+    a = dev(ctx, iota_diag(orc, 10))
+    eps = 1e-3
+    u = np.zeros(10)
+    u[2] = 1.0
+    u[7] = eps
+    norm = np.linalg.norm(u)
+    u /= norm
+    r = adp.compute_residuals_device(a, tcuda(u[:, None].copy()), [3.0])
+    assert r[0] == pytest.approx(eps * 5.0 / norm, rel=1e-12)
+
+
+# ------------------------------------------------------- CholQR2 / Rayleigh-Ritz ---
+def test_cholqr_orthonormal_and_span(ctx, orc):  # test_dense_kernels.cpp (CholQR2 <= 1e-12 on 500 x 40)
+    x = orc.fill_gaussian(500, 40, 3, 0)
+    xt = tcuda(x)
+    kept = adp.cholesky_qr_device(xt)
+    q = xt.cpu().numpy()
+    assert kept == 40
+    assert np.linalg.norm(q.T @ q - np.eye(40)) <= 1e-12
+    # same span: x = q (q^T x)
+    assert np.linalg.norm(x - q @ (q.T @ x)) <= 1e-10 * np.linalg.norm(x)
+
+
+def test_cholqr_drops_dependent_columns(ctx, orc):
+    x = orc.fill_gaussian(300, 10, 5, 0)
+    x[:, 7] = 2.0 * x[:, 1] - x[:, 3]  # dependent column -> MGS fallback drops it
+    xt = tcuda(x)
+    kept = adp.cholesky_qr_device(xt)
+    q = xt.cpu().numpy()[:, :kept]
+    assert kept == 9
+    assert np.linalg.norm(q.T @ q - np.eye(kept)) <= 1e-12
+
+
+def test_rayleigh_ritz_invariant_subspace(ctx, orc):
+    m = orc.random_symmetric(120, 0.1, 8)
+    w, v = np.linalg.eigh(m.to_dense())
+    q = v[:, 30:45].copy()
+    theta, vv = adp.rayleigh_ritz_device(dev(ctx, m), tcuda(q))
+    assert np.allclose(theta, w[30:45], rtol=0, atol=1e-11 * np.abs(w).max())
+    r = adp.compute_residuals_device(dev(ctx, m), vv, theta)
+    assert r.max() <= 1e-10 * np.abs(w).max()
+
+
+# ------------------------------------------------------------------------- solve ---
+def test_solve_diagonal_slice(ctx, orc):  # test_eigensolver.cpp:168-192
+    a = dev(ctx, iota_diag(orc, 100))
+    res = adp.solve(a, adp.SolverConfig(interval_a=10.5, interval_b=20.5, rng_seed=7, collect_diagnostics=True))
+    assert res.converged and len(res.eigenvalues) == 10
+    assert np.allclose(res.eigenvalues, np.arange(11, 21), rtol=1e-9, atol=0)
+    assert res.max_residual <= 1e-10 * 100.0 * 1.01
+    for i in range(10):
+        col = res.eigenvectors[:, i]
+        assert abs(np.abs(col).max() - 1.0) <= 1e-6 and np.linalg.norm(col) == pytest.approx(1.0)
+    for rec in res.history:
+        assert 0.0 <= rec.orth_error <= 1e-8
+
+
+def test_solve_empty_interval_short_circuits(ctx, orc):  # :194-204
+    res = adp.solve(dev(ctx, iota_diag(orc, 60)), adp.SolverConfig(interval_a=30.3, interval_b=30.7, rng_seed=3))
+    assert res.converged and len(res.eigenvalues) == 0 and res.iterations == 0
+
+
+def test_solve_empty_interval_forced_subspace(ctx, orc):  # :206-219
+    res = adp.solve(dev(ctx, iota_diag(orc, 60)),
+                    adp.SolverConfig(interval_a=30.3, interval_b=30.7, rng_seed=3, p_override=8))
+    assert res.converged and len(res.eigenvalues) == 0 and 10 <= res.iterations <= 15
+    assert all(r.e_in_interval == 0 for r in res.history)
+
+
+def test_solve_dense_fallback(ctx, orc):  # :221-236
+    m = orc.random_symmetric(30, 0.3, 55)
+    sp = spectrum(m)
+    res = adp.solve(dev(ctx, m), adp.SolverConfig(interval_a=sp[5] - 1e-9, interval_b=sp[24] + 1e-9, rng_seed=1,
+                                                  p_override=30))
+    assert res.dense_fallback and res.converged and len(res.eigenvalues) == 20
+    assert np.allclose(res.eigenvalues, sp[5:25], rtol=1e-12, atol=0)
+
+
+def test_solve_invalid_configs(ctx, orc):  # :238-253
+    a = dev(ctx, iota_diag(orc, 40))
+    for kw in (dict(interval_a=5.5, interval_b=5.0), dict(interval_a=200.0, interval_b=300.0),
+               dict(interval_a=5.0, interval_b=6.5, tau_c=0.0)):
+        with pytest.raises(adp.ConfigError):
+            adp.solve(a, adp.SolverConfig(**kw))
+
+
+def test_solve_max_iter(ctx, orc):  # :255-265
+    res = adp.solve(dev(ctx, iota_diag(orc, 100)),
+                    adp.SolverConfig(interval_a=10.5, interval_b=20.5, rng_seed=7, max_iter=2))
+    assert not res.converged and res.iterations == 2
+
+
+def test_solve_bitwise_deterministic(ctx, orc):  # :267-281
+    m = orc.random_symmetric(90, 0.08, 2)
+    sp = spectrum(m)
+    cfg = adp.SolverConfig(interval_a=sp[30] - 1e-3, interval_b=sp[40] + 1e-3, rng_seed=11)
+    a = dev(ctx, m)
+    r1, r2 = adp.solve(a, cfg), adp.solve(a, cfg)
+    assert np.array_equal(r1.eigenvalues, r2.eigenvalues) and r1.spmv_total == r2.spmv_total
+    assert r1.degree_history == r2.degree_history and np.array_equal(r1.eigenvectors, r2.eigenvectors)
+
+
+def test_solve_spmv_accounting(ctx, orc):  # :283-312
+    a = dev(ctx, iota_diag(orc, 100))
+    cfg = adp.SolverConfig(interval_a=10.5, interval_b=20.5, rng_seed=7)
+    res = adp.solve(a, cfg)
+    assert res.converged
+    setup = [0]
+    b = adp.estimate_spectrum_bounds(a, cfg.lanczos_steps, cfg.rng_seed, setup)
+    span = b.lambda_max - b.lambda_min
+    alpha = math.acos((2.0 * cfg.interval_a - b.lambda_max - b.lambda_min) / span)
+    beta = math.acos((2.0 * cfg.interval_b - b.lambda_max - b.lambda_min) / span)
+    k1 = adp.initial_degree(alpha, beta, cfg.c)
+    f = adp.build_filter(cfg.interval_a, cfg.interval_b, b, int(math.ceil(cfg.k_multiplier * k1)), cfg.m)
+    adp.estimate_eigcount(a, f, cfg.trace_probes, cfg.rng_seed, setup)
+    costs = 0
+    for rec in res.history:
+        assert rec.spmv_filter == rec.degree * rec.active_width
+        costs += rec.spmv_filter + rec.spmv_residual
+    assert res.spmv_total == setup[0] + costs + len(res.eigenvalues)
+
+
+def test_solve_locks_monotone(ctx, orc):  # :314-336
+    m = orc.random_symmetric(150, 0.06, 91)
+    sp = spectrum(m)
+    cfg = adp.SolverConfig(interval_a=0.5 * (sp[59] + sp[60]), interval_b=0.5 * (sp[74] + sp[75]), rng_seed=19)
+    res = adp.solve(dev(ctx, m), cfg)
+    assert res.converged and len(res.eigenvalues) == 15
+    prev = 0
+    for rec in res.history:
+        assert rec.n_locked_total >= prev
+        prev = rec.n_locked_total
+    a_norm = max(abs(res.bounds.lambda_min), abs(res.bounds.lambda_max))
+    assert res.max_residual <= 2.0 * cfg.tau_c * a_norm
+    assert np.all(np.abs(res.eigenvalues - sp[60:75]) <= 1e-8 * a_norm)
+
+
+def test_solve_oracle_sweep(ctx, orc):  # :338-366
+    exact = 0
+    for trial in range(8):
+        m = orc.random_symmetric(120, 0.07, 1000 + trial)
+        sp = spectrum(m)
+        rng = orc.MT19937_64(500 + trial)
+        count = rng.uniform_int(5, 15)
+        start = rng.uniform_int(20, 90)
+        lo = 0.5 * (sp[start - 1] + sp[start])
+        hi = 0.5 * (sp[start + count - 1] + sp[start + count])
+        res = adp.solve(dev(ctx, m), adp.SolverConfig(interval_a=lo, interval_b=hi, rng_seed=trial))
+        if not res.converged or len(res.eigenvalues) != count:
+            continue
+        a_norm = max(abs(sp[0]), abs(sp[-1]))
+        if np.all(np.abs(res.eigenvalues - sp[start:start + count]) <= 1e-8 * a_norm):
+            exact += 1
+    assert exact >= 7
+
+
+def test_spurious_safety(ctx, orc):  # :368-402
+    m = orc.random_symmetric(80, 0.15, 61)
+    sp = spectrum(m)
+    lo, hi = sp[25], sp[55]
+    a = dev(ctx, m)
+    for seed in range(10):
+        xt = tcuda(orc.fill_gaussian(80, 15, seed, 4))
+        kept = adp.cholesky_qr_device(xt)
+        theta, v = adp.rayleigh_ritz_device(a, xt[:, :kept].contiguous())
+        idx = [j for j in range(len(theta)) if lo <= theta[j] <= hi]
+        if not idx:
+            continue
+        lin = theta[idx]
+        r = adp.compute_residuals_device(a, v[:, idx].contiguous(), lin)
+        tau_s = adp.spurious_threshold(lin, lo, hi)
+        for c in range(len(lin)):
+            if r[c] >= tau_s:
+                continue
+            inside = sp[(sp >= lo) & (sp <= hi)]
+            assert np.any(np.abs(lin[c] - inside) <= r[c] * (1.0 + 1e-12))
+
+
+def test_solve_spurious_detection_off(ctx, orc):  # :404-414
+    res = adp.solve(dev(ctx, iota_diag(orc, 50)),
+                    adp.SolverConfig(interval_a=10.5, interval_b=20.5, rng_seed=5, spurious_detection=False))
+    assert res.converged and len(res.eigenvalues) == 10
