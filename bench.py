@@ -53,6 +53,7 @@ def parse_args():
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve (second half of the metric)")
     p.add_argument("--panel", type=int, default=0)
     p.add_argument("--variant", type=int, default=0)
     return p.parse_args()
@@ -195,6 +196,44 @@ def run_reference(args):
     return 0
 
 
+def end_to_end_solve(adp, configs, ctx, with_cpu: bool):
+    """End-to-end solve time (the metric's second half) on config 1 with the narrowed window (c1s).
+
+    GPU: wall time of adp.solve (setup + loop, stage split). CPU: a projection -- the oracle's
+    measured time per degree step (the reference's maspmm + update) x the GPU run's filter work
+    (sum of degree x active width, plus the k_max x 30-probe trace estimate), labelled as such.
+    """
+    import torch
+
+    cfg = configs.CONFIGS["c1s"]
+    a = cfg.operator()
+    da = adp.DeviceCsr(a, ctx)
+    scfg = adp.SolverConfig(interval_a=cfg.window[0], interval_b=cfg.window[1], rng_seed=0)
+    adp.solve(da, scfg)  # warm (workspace, handles)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = adp.solve(da, scfg)
+    torch.cuda.synchronize()
+    gpu_s = time.perf_counter() - t0
+    out = {"config": "c1s: " + cfg.description, "n": a.n_rows, "window": list(cfg.window),
+           "gpu_seconds": round(gpu_s, 4), "converged": res.converged, "n_eigs": int(len(res.eigenvalues)),
+           "iterations": res.iterations, "spmv_total": res.spmv_total, "avg_degree": round(res.avg_degree, 1),
+           "max_residual": res.max_residual, "subspace_dim": res.subspace_dim,
+           "stage_seconds": {k: round(v, 4) for k, v in vars(res.timings).items()}}
+    if with_cpu:
+        # columns x degree-steps of filter work in the GPU run, including the setup trace estimate
+        k1 = configs.filter_degree(configs.Config("tmp", "", 0, cfg.window,
+                                                  (res.bounds.lambda_min, res.bounds.lambda_max), "f64", None))
+        k_max = max(k1, int(math.ceil(2.5 * k1)))
+        col_steps = k_max * 30 + sum(r.degree * r.active_width for r in res.history)
+        sec, steps, threads = cpu_sample(a, 64, 4.0)
+        per_col_step = sec / steps / 64
+        out["cpu_projected_seconds"] = round(col_steps * per_col_step, 2)
+        out["cpu_projection"] = (f"oracle degree-step time ({steps} steps at q=64, {threads} threads: "
+                                 f"{1e3 * sec / steps:.2f} ms) x {col_steps} column-steps of the GPU run's filter work")
+    return out
+
+
 # ------------------------------------------------------------- GPU arm ---
 def run_ours(args):
     import torch
@@ -309,6 +348,10 @@ def run_ours(args):
                "d2h_bytes_per_step": n * q * 8, "ms_per_step": round(t_e2e * 1e3, 3), "matches_device_result": same,
                "api": "adp_filter_apply (C-ABI, host column-major, pinned)"}
 
+    solve_info = None
+    if rank == 0 and not args.no_solve:
+        solve_info = end_to_end_solve(adp, configs, ctx, with_cpu=(world == 1 and not args.no_cpu_baseline))
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sec, steps, threads = cpu_sample(a, q, args.cpu_seconds)
@@ -337,6 +380,7 @@ def run_ours(args):
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "solve": solve_info,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -161,6 +161,12 @@ CONFIGS = {
     "c3": Config("c3", "2D Peierls lattice 1000^2, phi=1/64, on-site U[-1,1], complex128, q=384", 384,
                  (-0.0005, 0.0005), (-5.0, 5.0), "c128",
                  lambda: peierls_lattice(1000)),
+    # Config 1 for END-TO-END solves: the literal 0.40-0.45 window holds ~6,000 eigenvalues against block 64
+    # (p >= e is violated); this window is centred at 0.425 of the range and narrowed to
+    # ~35 eigenvalues, so the reference rule p = max(ceil(1.8 e), e + 5, 10) applies.
+    "c1s": Config("c1s", "3D 7-pt Laplacian 40^3 + U[0,1) potential, solve window ~35 eigenvalues", 64,
+                  (0.425 * 13.0 - 0.002, 0.425 * 13.0 + 0.002), (0.0, 13.0), "f64",
+                  lambda: laplacian7_potential(40, 0.0, 1.0)),
     "c4": Config("c4", "3D 27-pt Mehrstellen 128^3 + Gaussian-sum potential, q=1024", 1024,
                  (0.30, 0.32), (-2.0, 8.6), "f64",
                  lambda: dft_like_27pt(128)),
