@@ -145,8 +145,10 @@ const Tiling* get_tiling(adp_csr* a, int64_t panel_bytes, int64_t stage_bytes);
 // Launches the tiled kernel for the step; returns false if the operator cannot
 // be tiled for this width (the caller then uses the row kernel).
 bool launch_step_tiled(adp_ctx* ctx, StepMode mode, const StepArgs& args);
-// The persistent software-pipelined row kernel (cheb_row.cu), default for wide blocks.
+// The persistent software-pipelined row kernel (cheb_row.cu; tuning variants).
 bool launch_step_row(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+// The default lean kernel (cheb_lean.cu) for >= 4 vectors per row.
+bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 
 // Host filter helpers (filter_host.cpp).
 std::vector<double> step_coeffs(double alpha, double beta, int k);

@@ -407,183 +407,16 @@ void launch_ch(adp_ctx* ctx, StepMode mode, RArgs k) {
 }
 
 
-// ---- lean one-task-per-warp kernel ---------------------------------------------
-// Full panels only (q a multiple of the panel width): no per-vector predicates,
-// 32-bit index math and one IMAD.WIDE per gathered row -- about 25 SASS
-// instructions per nonzero instead of ~150 (the profile showed the first
-// version issue-bound on predicated 64-bit address arithmetic).
-template <class F, int CH, int U, int MODE, class RP, int MINB, bool HINT>
-__global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const RArgs p) {
-  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
-  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
-  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
-  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
-  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
-  using Val = typename F::Val;
-  extern __shared__ double2 ring[];  // [warp][V, Y][CH][32]
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t nrows = static_cast<int32_t>(p.nrows);
-  const int32_t task = static_cast<int32_t>(blockIdx.x) * kWarps + warp;
-  if (task >= nrows * static_cast<int32_t>(p.n_panels)) return;
-  const int32_t panel = task / nrows;
-  const int64_t r = p.row_begin + (task - panel * nrows);
-  const uint32_t voff = (static_cast<uint32_t>(panel) * (32 * CH) + lane) * 16u;  // byte offset in a row
-  const uint32_t ldg_b = static_cast<uint32_t>(p.ldv) * 16u;
-  const char* gb = reinterpret_cast<const char*>(p.g) + voff;
-  const uint64_t pol = policy_evict_first_rt(p.pol_frac);
-
-  // V[r], Y[r] panels arrive by TMA bulk copies (lane 0, L2 evict-first hint)
-  // into this warp's shared-memory slot, completing on the warp's mbarrier.
-  // The epilogue operands V[r], Y[r] arrive by TMA bulk copies (lane 0, L2
-  // evict-first hint) into this warp's shared-memory slot, completing on the
-  // warp's mbarrier. (The own W row stays an L1-hit __ldg: staging it too
-  // grew the carve-out and cost more in L1 hits than it saved -- measured.)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ring) + warp;
-  double2* my = ring + 8 + warp * (2 * CH * 32);  // 8 x 16 B header holds the 8 mbarriers
-  constexpr uint32_t kPB = 32u * CH * 16u;
-  if constexpr (kStep) {
-    if (lane == 0) {
-      mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
-      const char* vsrc = reinterpret_cast<const char*>(p.vin) + static_cast<uint64_t>(r) * ldg_b + poff;
-      const char* ysrc = reinterpret_cast<const char*>(p.yin) + static_cast<uint64_t>(r) * (static_cast<uint32_t>(p.ldyv) * 16u) + poff;
-      mbar_arrive_expect_tx(bar, 2 * kPB);
-      bulk_g2s_hint(my, vsrc, kPB, bar, pol);
-      bulk_g2s_hint(my + CH * 32, ysrc, kPB, bar, pol);
-    }
-  }
-  const char* ob = reinterpret_cast<char*>(p.out) + static_cast<uint64_t>(r) * (static_cast<uint32_t>(p.ldo) * 16u) + voff;
-
-  double2 acc[CH];
-#pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    if constexpr (kSpmmAcc)
-      acc[c] = *reinterpret_cast<const double2*>(ob + 512 * c);
-    else
-      acc[c] = make_double2(0.0, 0.0);
-  }
-  const RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r));
-  const RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r + 1));
-  for (RP e = start; e < end; e += U) {
-    int cidx[U];
-    Val v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (e + u < end) {
-        cidx[u] = __ldg(p.col + e + u);
-        v[u] = F::load(p.val, static_cast<int64_t>(e) + u);
-      }
-    }
-    double2 w[U][CH];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (e + u < end) {
-        const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx[u])) * ldg_b);
-#pragma unroll
-        for (int c = 0; c < CH; ++c) w[u][c] = __ldg(src + 32 * c);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (e + u < end) {
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          double2 wv = w[u][c];
-          if constexpr (kFirst) wv = scale2(p.s2, wv);
-          acc[c] = F::mac(acc[c], v[u], wv);
-        }
-      }
-    }
-  }
-  if constexpr (kStep) {
-    __syncwarp();
-    mbar_wait(bar, 0);
-  }
-  const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * ldg_b);
-  char* wb = kFirst ? reinterpret_cast<char*>(p.wout) + static_cast<uint64_t>(r) * (static_cast<uint32_t>(p.ldo) * 16u) + voff : nullptr;
-#pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    double2 own = make_double2(0.0, 0.0);
-    if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
-    double2 res;
-    if constexpr (kStep) {
-      const double2 vv = my[(0 * CH + c) * 32 + lane];
-      const double2 yy = my[(1 * CH + c) * 32 + lane];
-      res = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
-    } else if constexpr (kFirst) {
-      const double2 wn = scale2(p.s2, own);
-      if constexpr (HINT) st_hint(reinterpret_cast<double2*>(wb + 512 * c), wn, pol);
-      else *reinterpret_cast<double2*>(wb + 512 * c) = wn;
-      res = add2(scale2(p.s0, acc[c]), scale2(p.s1, wn));
-    } else if constexpr (kDeg1) {
-      res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own))));
-    } else {
-      res = acc[c];
-    }
-    if constexpr (HINT) st_hint(reinterpret_cast<double2*>(const_cast<char*>(ob) + 512 * c), res, pol);
-    else *reinterpret_cast<double2*>(const_cast<char*>(ob) + 512 * c) = res;
-  }
-}
-
-template <class F, int CH, int U, class RP, int MINB>
-void launch_lean(adp_ctx* ctx, StepMode mode, RArgs k) {
-  k.n_panels = k.qv / (32 * CH);
-  const int64_t total = k.nrows * k.n_panels;
-  if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_lean: too many tasks");
-  const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
-  const size_t smem = mode == StepMode::Step ? 128 + static_cast<size_t>(kWarps) * 2 * CH * 32 * 16 : 16;
-  auto run = [&](auto kern) {
-    if (smem > 48 * 1024)
-      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, kThreads, smem, ctx->stream>>>(k);
-  };
-  static const bool nohint = std::getenv("ADP_LEAN_NOHINT") != nullptr;
-  if (nohint) {
-    switch (mode) {
-      case StepMode::First: run(cheb_lean_kernel<F, CH, U, 0, RP, MINB, false>); break;
-      case StepMode::Step: run(cheb_lean_kernel<F, CH, U, 1, RP, MINB, false>); break;
-      case StepMode::Deg1: run(cheb_lean_kernel<F, CH, U, 2, RP, MINB, false>); break;
-      case StepMode::Spmm: run(cheb_lean_kernel<F, CH, U, 3, RP, MINB, false>); break;
-      case StepMode::SpmmAcc: run(cheb_lean_kernel<F, CH, U, 4, RP, MINB, false>); break;
-    }
-  } else {
-    switch (mode) {
-      case StepMode::First: run(cheb_lean_kernel<F, CH, U, 0, RP, MINB, true>); break;
-      case StepMode::Step: run(cheb_lean_kernel<F, CH, U, 1, RP, MINB, true>); break;
-      case StepMode::Deg1: run(cheb_lean_kernel<F, CH, U, 2, RP, MINB, true>); break;
-      case StepMode::Spmm: run(cheb_lean_kernel<F, CH, U, 3, RP, MINB, true>); break;
-      case StepMode::SpmmAcc: run(cheb_lean_kernel<F, CH, U, 4, RP, MINB, true>); break;
-    }
-  }
-  ADP_LAUNCH_CHECK();
-  ctx->launches += 1;
-}
-
 template <class F, class RP>
 void dispatch_row(adp_ctx* ctx, StepMode mode, const RArgs& k, int pipe_variant) {
-  // tuning variants (adp_ctx_set_tuning 11..15): lean kernel geometry (CH, U, MINB)
+  // tuning variants (adp_ctx_set_tuning 11..15) of the persistent pipelined kernel
   switch (pipe_variant) {
-    case 1: if (k.qv % 32 == 0) { launch_lean<F, 1, 1, RP, 8>(ctx, mode, k); return; } break;
-    case 2: if (k.qv % 32 == 0) { launch_lean<F, 1, 4, RP, 6>(ctx, mode, k); return; } break;
-    case 3: if (k.qv % 64 == 0) { launch_lean<F, 2, 1, RP, 6>(ctx, mode, k); return; } break;
-    case 4: if (k.qv % 128 == 0) { launch_lean<F, 4, 4, RP, 2>(ctx, mode, k); return; } break;
-    case 5: if (k.qv % 64 == 0) { launch_lean<F, 2, 2, RP, 5>(ctx, mode, k); return; } break;
-    default: break;
+    case 1: return launch_ch<F, RP, 4, 4, 2>(ctx, mode, k);
+    case 2: return launch_ch<F, RP, 2, 8, 2>(ctx, mode, k);
+    case 3: return launch_ch<F, RP, 2, 4, 3>(ctx, mode, k);
+    case 4: return launch_ch<F, RP, 3, 4, 2>(ctx, mode, k);
+    default: return launch_ch<F, RP, 2, 4, 3>(ctx, mode, k);
   }
-  // automatic: lean kernel on full panels (widest of 4 / 2 / 1 vectors per lane), else pipelined
-  // (measured on config 2: one gathered row in flight per warp and more resident
-  //  warps beats deeper per-warp batches -- CH 4, U 1, 4 blocks/SM: 83% of HBM)
-  if (k.qv % 128 == 0) return launch_lean<F, 4, 1, RP, 4>(ctx, mode, k);
-  if (k.qv % 64 == 0) return launch_lean<F, 2, 1, RP, 6>(ctx, mode, k);
-  if (k.qv % 32 == 0) return launch_lean<F, 1, 1, RP, 8>(ctx, mode, k);
-  const int64_t n4 = (k.qv + 127) / 128;
-  const int64_t ch = ((k.qv + n4 - 1) / n4 + 31) / 32;
-  if (ch >= 4) launch_ch<F, RP, 4, 4, 2>(ctx, mode, k);
-  else if (ch == 3) launch_ch<F, RP, 3, 4, 2>(ctx, mode, k);
-  else if (ch == 2) launch_ch<F, RP, 2, 8, 2>(ctx, mode, k);
-  else launch_ch<F, RP, 2, 4, 3>(ctx, mode, k);
 }
 
 }  // namespace

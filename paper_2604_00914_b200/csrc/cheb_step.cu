@@ -387,11 +387,14 @@ void launch_step(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
       (s.wout && !aligned(s.wout)))
     fail(ADP_ERR_DIMENSION, "cheb_step: operands must be 16-byte aligned");
   if (s.row_end <= s.row_begin || s.q == 0) return;
-  // B200 path: the TMA-pipelined tile kernel (cheb_tile.cu). Variants 1-7 force
-  // the row kernel below (tuning comparisons); it also serves thin blocks and
-  // operators whose rows do not fit a shared-memory stage.
+  // Dispatch: the lean kernel (cheb_lean.cu) is the default for >= 4 vectors
+  // (ragged widths split into full-panel launches); the TMA tile kernel
+  // (cheb_tile.cu) when its knobs are set; the persistent pipelined row kernel
+  // (cheb_row.cu) and this file's one-row-per-group kernel as tuning variants
+  // and for 1-3 vectors.
   if (ctx->tile_ch > 0 && launch_step_tiled(ctx, mode, s)) return;
-  if ((ctx->variant == 0 || ctx->variant > 10) && launch_step_row(ctx, mode, s)) return;
+  if (ctx->variant == 0 && launch_step_lean(ctx, mode, s)) return;
+  if (ctx->variant > 10 && launch_step_row(ctx, mode, s)) return;
   KArgs k{};
   k.row_ptr = a->row_ptr;
   k.col = a->col_idx;

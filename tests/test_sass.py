@@ -48,7 +48,8 @@ def test_tma_and_async_copies_present(sass):
     _, funcs = sass
     tile = [f for f in funcs if "cheb_tile_kernel" in f]
     assert tile and all(any("UBLKCP" in ln for ln in funcs[f]) for f in tile if "ELi1EEEv" in f)
-    lean_step = [f for f in funcs if "cheb_lean_kernel" in f and re.search(r"ELi1E[il]Li\dELb", f)]
+    # cheb_lean_kernel<F, G, CH, U, MODE=1 (Step), RP, MINB>
+    lean_step = [f for f in funcs if re.search(r"cheb_lean_kernelI\w+?ELi\d+ELi\d+ELi\d+ELi1E[il]Li\d+E", f)]
     assert lean_step and all(any("UBLKCP" in ln for ln in funcs[f]) for f in lean_step)
     row_step = [f for f in funcs if "cheb_row_kernel" in f and re.search(r"ELi1E[il]Li\dELb", f)]
     assert row_step and all(any("LDGSTS" in ln for ln in funcs[f]) for f in row_step)

@@ -25,10 +25,11 @@ def main():
     p.add_argument("--variants", default="1", help="row-kernel variants (1-7); 0 = automatic")
     p.add_argument("--tiles", default="", help="tile configs 'ch,stages,kib,ctas;...' (0 = default)")
     p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--q", type=int, default=0, help="override the block width")
     args = p.parse_args()
     cfg = configs.CONFIGS[args.config]
     a = cfg.operator()
-    n, nnz, q = a.n_rows, a.nnz, cfg.q
+    n, nnz, q = a.n_rows, a.nnz, (args.q or cfg.q)
     k1 = configs.filter_degree(cfg)
     f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, max(args.degree, int(math.ceil(2.5 * k1))), 0.5)
     ctx = adp.Context(0)
