@@ -263,10 +263,10 @@ void launch_lean(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
 // measured on configs 1-2 (tools/tune_step.py): widest panel with one gathered
 // row in flight per group and many resident warps.
 template <class F, class RP>
-void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv) {
-  if (qv % 128 == 0) return launch_lean<F, 32, 4, 1, RP, 4>(ctx, mode, k, qv);
-  if (qv % 64 == 0) return launch_lean<F, 32, 2, 1, RP, 6>(ctx, mode, k, qv);
-  if (qv % 32 == 0) return launch_lean<F, 32, 1, 1, RP, 8>(ctx, mode, k, qv);
+void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_t cap) {
+  if (qv % 128 == 0 && cap >= 128) return launch_lean<F, 32, 4, 1, RP, 4>(ctx, mode, k, qv);
+  if (qv % 64 == 0 && cap >= 64) return launch_lean<F, 32, 2, 1, RP, 6>(ctx, mode, k, qv);
+  if (qv % 32 == 0 && cap >= 32) return launch_lean<F, 32, 1, 1, RP, 8>(ctx, mode, k, qv);
   if (qv % 16 == 0) return launch_lean<F, 16, 1, 1, RP, 8>(ctx, mode, k, qv);
   if (qv % 8 == 0) return launch_lean<F, 8, 1, 1, RP, 8>(ctx, mode, k, qv);
   return launch_lean<F, 4, 1, 1, RP, 8>(ctx, mode, k, qv);  // qv % 4 == 0
@@ -303,11 +303,16 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   k.s3 = s.s3;
   if (k.nrows >= (int64_t{1} << 30)) return false;
   // ragged widths: split into full-panel launches on column-offset pointers
+  // panel cap (adp_ctx_set_panel): narrower panels shrink the L2 footprint of the
+  // stencil's W reuse window at the cost of re-reading A once per panel
+  const int64_t cap = ctx->panel_cols > 0 ? std::max<int64_t>(4, ctx->panel_cols / epv) : 128;
   int64_t done = 0;
   while (qv - done >= 4) {
     const int64_t rem = qv - done;
     int64_t take;
-    if (rem >= 128) take = (rem / 128) * 128;
+    if (rem >= 128 && cap >= 128) take = (rem / 128) * 128;
+    else if (rem >= 64 && cap >= 64) take = (rem / 64) * 64;
+    else if (rem >= 32 && cap >= 32) take = (rem / 32) * 32;
     else if (rem >= 64) take = 64;
     else if (rem >= 32) take = 32;
     else if (rem >= 16) take = 16;
@@ -321,11 +326,11 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
     kk.out += off;
     kk.wout = k.wout ? k.wout + off : nullptr;
     if (cplx) {
-      if (a->rp64) launch_full<CplxL, int64_t>(ctx, mode, kk, take);
-      else launch_full<CplxL, int32_t>(ctx, mode, kk, take);
+      if (a->rp64) launch_full<CplxL, int64_t>(ctx, mode, kk, take, cap);
+      else launch_full<CplxL, int32_t>(ctx, mode, kk, take, cap);
     } else {
-      if (a->rp64) launch_full<RealL, int64_t>(ctx, mode, kk, take);
-      else launch_full<RealL, int32_t>(ctx, mode, kk, take);
+      if (a->rp64) launch_full<RealL, int64_t>(ctx, mode, kk, take, cap);
+      else launch_full<RealL, int32_t>(ctx, mode, kk, take, cap);
     }
     done += take;
   }

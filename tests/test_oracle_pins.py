@@ -473,3 +473,35 @@ def test_golden_fixture_outputs_reproduce(orc, golden_dir):
         t = orc.Tiled(a, 256, 64)
         for d in (0, 1, 2, 3, 17, 40):
             assert np.array_equal(orc.clenshaw_apply(f, t, z[f"{name}/x"], d), z[f"{name}/deg{d}"])
+
+
+# ------------------------------------------- complex128: real-embedding pin ---
+def test_complex_oracle_pinned_by_real_embedding(orc):
+    # No reference exists for complex Hermitian input. The complex
+    # restatement is pinned by the real embedding S = [[A, -B], [B, A]] of H = A + iB:
+    # rho(S) [Re X; Im X] = [Re rho(H) X; Im rho(H) X].
+    rng = np.random.default_rng(7)
+    n, q = 120, 5
+    mask = np.triu(rng.random((n, n)) < 0.06)
+    h = np.where(mask, rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)), 0)
+    h = h + np.conj(np.triu(h, 1)).T
+    h[np.diag_indices(n)] = h[np.diag_indices(n)].real
+    s = np.block([[h.real, -h.imag], [h.imag, h.real]])
+
+    def csr_of(d):
+        r, c = np.nonzero(d)
+        return orc.Csr(d.shape[0], d.shape[1],
+                       np.concatenate([[0], np.cumsum(np.bincount(r, minlength=d.shape[0]))]).astype(np.int64),
+                       c.astype(np.int64), d[r, c])
+
+    hc, sc = csr_of(h), csr_of(s)
+    ev = np.linalg.eigvalsh(h)
+    bounds = (ev[0] - 0.1, ev[-1] + 0.1)
+    f = orc.build_filter(ev[30], ev[60], bounds, 50, 0.5)
+    x = rng.standard_normal((n, q)) + 1j * rng.standard_normal((n, q))
+    for d in (0, 1, 2, 7, 50):
+        got = orc.clenshaw_apply(f, orc.Tiled(hc, 256, 64), x, d)
+        emb = orc.clenshaw_apply(f, orc.Tiled(sc, 256, 64), np.vstack([x.real, x.imag]), d)
+        assert rel_fro(got, emb[:n] + 1j * emb[n:]) <= 1e-12
+    # and the eigenvalues of S are those of H, each doubled
+    assert np.allclose(np.linalg.eigvalsh(s)[::2], ev, atol=1e-10)

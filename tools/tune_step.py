@@ -26,6 +26,7 @@ def main():
     p.add_argument("--tiles", default="", help="tile configs 'ch,stages,kib,ctas;...' (0 = default)")
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--q", type=int, default=0, help="override the block width")
+    p.add_argument("--panels", default="", help="lean-kernel panel caps in columns, e.g. '128,256'")
     args = p.parse_args()
     cfg = configs.CONFIGS[args.config]
     a = cfg.operator()
@@ -43,7 +44,13 @@ def main():
     runs = [("row", int(s), None) for s in args.variants.split(",") if s]
     for spec in filter(None, args.tiles.split(";")):
         runs.append(("tile", 0, [int(x) for x in spec.split(",")]))
+    for spec in filter(None, args.panels.split(",")):
+        runs.append(("panel", int(spec), None))
     for kind, v, tcfg in runs:
+        ctx_panel = v if kind == "panel" else 0
+        ctx.set_panel(ctx_panel)
+        if kind == "panel":
+            v = 0
         ctx.set_tuning(v)
         ctx.set_tile_config(*(tcfg or [0, 0, 0, 0]))
         y = torch.empty_like(x)
@@ -61,7 +68,7 @@ def main():
             ref = y.clone()
         else:
             same = bool(torch.equal(ref, y))
-        label = f"variant {v}" if kind == "row" else f"tile ch,stages,kib,ctas={tcfg}"
+        label = {"row": f"variant {v}", "panel": f"lean panel cap {ctx_panel}"}.get(kind, f"tile ch,stages,kib,ctas={tcfg}")
         print(f"{args.config} q={q} {label}: {ms:.4f} ms/launch  {b_step / ms / 1e6:.1f} GB/s  "
               f"bitwise_vs_first={same}", flush=True)
 
