@@ -257,6 +257,8 @@ def run_ours(args):
     degree = args.degree or k1
     k_max = max(degree, int(math.ceil(2.5 * k1)))
     f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, k_max, 0.5)
+    if world > 1:
+        return run_distributed(args, adp, cfg, a, f, degree, rank, world, device)
 
     ctx = adp.Context(device)
     if args.panel:
@@ -385,6 +387,77 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_distributed(args, adp, cfg, a, f, degree, rank, world, device):
+    """N > 1: the filter row-partitioned over the ranks (strong scaling: the operator is fixed),
+    halo rows exchanged per degree step over NCCL while interior rows compute
+    (paper_2604_00914_b200/distributed.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_00914_b200.distributed import CudaStepBackend, DistributedFilter
+
+    n, nnz, q = a.n_rows, a.nnz, cfg.q
+    ctx = adp.Context(device)
+    be = CudaStepBackend(ctx)
+    df = DistributedFilter(a, be, rank, world)
+    r0, r1 = df.ranges[rank]
+    g = torch.Generator(device="cuda").manual_seed(rank)
+    x = torch.randn(r1 - r0, q, dtype=torch.float64, device="cuda", generator=g)
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        df.apply(f.coeffs, f.l1, f.l2, x, degree)
+    barrier()
+    clocks = ClockSampler(device)
+    clocks.start()
+    launches0 = ctx.launch_count
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record()
+    for _ in range(args.steps):
+        y = df.apply(f.coeffs, f.l1, f.l2, x, degree)
+    ev1.record()
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    bytes_call = call_bytes(n, nnz, q, degree)
+    value = bytes_call / (ms_step * 1e-3) / 1e9
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            yh = df.apply(f.coeffs, f.l1, f.l2, xh.to("cuda", non_blocking=True), degree).to("cpu")
+        barrier()
+        te = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(bytes_call / float(te.item()) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": n * q * 8, "d2h_bytes_per_step": n * q * 8,
+               "api": "DistributedFilter.apply (host tensors in/out)"}
+    peak, peak_src = peaks()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg.description}; clenshaw_apply degree {degree}, "
+                                   f"rows partitioned over {world} GPUs, halo exchange per degree step",
+                       "n": n, "nnz": nnz, "q": q, "degree": degree, "bytes_per_step": bytes_call,
+                       "l2": "inputs larger than L2", "parallelism": f"row-partition x{world} (NCCL halo)"},
+            "pct_of_hbm_peak_per_gpu": round(100.0 * value / world / peak, 2),
+            "gpu_launches": ctx.launch_count - launches0, "clocks": clk, "e2e": e2e, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
     return 0
 
 

@@ -110,6 +110,20 @@ adp_status adp_filter_apply_device(adp_ctx* ctx, const adp_csr* a, const double*
                                    double l2, int32_t degree, const void* dx, int64_t x_rows, int64_t ldx, int64_t q,
                                    void* dy, int64_t ldy, int64_t* spmv_count);
 
+/* One fused Clenshaw degree step on device row-major blocks, for drivers that
+ * interleave steps with halo exchanges (multi-GPU row partition). mode:
+ *   0 FIRST  w = s2*g[r] -> wout, out = s0*(A*(s2*g)) + s1*w     (cheb_filter.cpp:162-165)
+ *   1 STEP   out = ((s0*(A*g) + s1*g[r]) - vin) + s2*yin          (cheb_filter.cpp:170-171,176-177)
+ *   2 DEG1   out = s0*g[r] + s1*(s2*(A*g) + s3*g[r])              (cheb_filter.cpp:154)
+ *   3 SPMM   out = A*g ;  4 SPMM_ACC out += A*g                   (tiled_matrix.hpp:184-210)
+ * Rows [row_begin, row_end) of A; output row r lives at out + r*ld_out; the own
+ * row of the gathered operand g is row r + goff (halo-extended layouts); all
+ * column indices of A index rows of g. Stream-ordered, no synchronisation. */
+adp_status adp_step_device(adp_ctx* ctx, const adp_csr* a, int32_t mode, const void* g, int64_t ld,
+                           const void* vin, const void* yin, int64_t ld_y, void* out, void* wout, int64_t ld_out,
+                           int64_t q, int64_t row_begin, int64_t row_end, int64_t goff, double s0, double s1,
+                           double s2, double s3);
+
 /* maspmm (include/adapoly/tiled_matrix.hpp:184-186): C += A B (accumulate != 0)
  * or C = A B (accumulate == 0; the reference's set_zero() + maspmm). Host
  * operands in the given layout; k = columns of B. */

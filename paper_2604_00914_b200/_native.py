@@ -87,6 +87,7 @@ SIGNATURES = {
     "adp_csr_info": (I32, [P, P, P, P, P]),
     "adp_filter_apply": (I32, [P, P, P, I32, D, D, I32, P, I64, I64, I64, I32, P, I64, P]),
     "adp_filter_apply_device": (I32, [P, P, P, I32, D, D, I32, P, I64, I64, I64, P, I64, P]),
+    "adp_step_device": (I32, [P, P, I32, P, I64, P, P, I64, P, P, I64, I64, I64, I64, I64, D, D, D, D]),
     "adp_spmm": (I32, [P, P, P, I64, I64, I64, I32, P, I64, I32]),
     "adp_spmm_device": (I32, [P, P, P, I64, I64, I64, P, I64, I32]),
     "adp_step_coeffs": (I32, [D, D, I32, P]),

@@ -408,6 +408,39 @@ adp_status adp_filter_apply(adp_ctx* ctx, const adp_csr* a, const double* coeffs
   });
 }
 
+adp_status adp_step_device(adp_ctx* ctx, const adp_csr* a, int32_t mode, const void* g, int64_t ld,
+                           const void* vin, const void* yin, int64_t ld_y, void* out, void* wout, int64_t ld_out,
+                           int64_t q, int64_t row_begin, int64_t row_end, int64_t goff, double s0, double s1,
+                           double s2, double s3) {
+  return guarded([&] {
+    if (mode < 0 || mode > 4) fail(ADP_ERR_CONFIG, "adp_step_device: unknown mode");
+    if (row_begin < 0 || row_end > a->n_rows || row_begin > row_end)
+      fail(ADP_ERR_DIMENSION, "adp_step_device: row range outside the operator");
+    if (q < 0 || ld < q || ld_out < q || (mode == 1 && ld_y < q))
+      fail(ADP_ERR_DIMENSION, "adp_step_device: leading dimension smaller than q");
+    set_device(ctx);
+    StepArgs s{};
+    s.a = a;
+    s.gsrc = g;
+    s.vin = vin;
+    s.yin = yin;
+    s.out = out;
+    s.wout = wout;
+    s.ld = ld;
+    s.ld_y = mode == 1 ? ld_y : ld;
+    s.ld_out = ld_out;
+    s.q = q;
+    s.row_begin = row_begin;
+    s.row_end = row_end;
+    s.goff = goff;
+    s.s0 = s0;
+    s.s1 = s1;
+    s.s2 = s2;
+    s.s3 = s3;
+    launch_step(ctx, static_cast<StepMode>(mode), s);
+  });
+}
+
 adp_status adp_spmm_device(adp_ctx* ctx, const adp_csr* a, const void* db, int64_t b_rows, int64_t ldb, int64_t k,
                            void* dc, int64_t ldc, int32_t accumulate) {
   return guarded([&] {

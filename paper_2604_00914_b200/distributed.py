@@ -1,0 +1,269 @@
+"""Multi-GPU row partition of the Chebyshev filter with per-degree halo exchange.
+
+The reference is single-process; the paper only describes a
+row-partitioned MPI layout. Here one process drives one GPU:
+
+* rank k owns a contiguous row range [r0, r1) of A and of the n x q blocks;
+* its CSR keeps only those rows, with columns re-indexed into a halo-extended
+  local layout  [halo_lo | own rows | halo_hi]  covering [cmin, cmax] (the
+  contiguous superset of the columns the rows touch -- exact for banded and
+  stencil operators); own row r sits at local row r + goff, goff = r0 - cmin;
+* the Clenshaw recurrence (proj/src/cheb_filter.cpp:162-177) runs step by step:
+  before each degree step the boundary rows of the current W that neighbours
+  need are exchanged (point-to-point send/recv through torch.distributed: NCCL
+  over NVLink on GPUs, gloo on CPU), while the INTERIOR rows -- whose columns
+  are all local -- are computed on the compute stream; the boundary rows are
+  computed once the halo has landed;
+* every rank's arithmetic is the single-GPU kernel's, in the same per-row
+  order, so the gathered distributed result is bitwise identical to the
+  single-process result (tests/test_distributed_cpu.py, tests/test_gpu_parity.py).
+
+The per-step kernel comes from a backend: ``CudaStepBackend`` (the C-ABI
+``adp_step_device`` on torch CUDA tensors) in the product; the CPU test suite
+plugs in a numpy restatement of the same step to exercise this driver under
+gloo.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .sparse import CsrMatrix
+
+FIRST, STEP, DEG1, SPMM, SPMM_ACC = 0, 1, 2, 3, 4
+
+
+def partition_rows(a: CsrMatrix, world: int) -> list[tuple[int, int]]:
+    """Contiguous row ranges balancing nonzeros + rows (the step streams both)."""
+    n = a.n_rows
+    work = np.diff(a.row_ptr).astype(np.float64) + 1.0
+    csum = np.concatenate([[0.0], np.cumsum(work)])
+    cuts = [0]
+    for k in range(1, world):
+        cuts.append(int(np.searchsorted(csum, csum[-1] * k / world)))
+    cuts.append(n)
+    return [(cuts[k], cuts[k + 1]) for k in range(world)]
+
+
+@dataclass
+class LocalPart:
+    """Rank-local slice of A with its halo layout and exchange schedule."""
+
+    rank: int
+    world: int
+    r0: int
+    r1: int
+    cmin: int
+    cmax: int
+    csr: CsrMatrix  # local rows, columns re-indexed to cmin-based local rows
+    interior: tuple[int, int]  # local row range whose columns are all owned
+    sends: dict = field(default_factory=dict)  # peer -> (global lo, hi) of MY rows the peer needs
+    recvs: dict = field(default_factory=dict)  # peer -> (global lo, hi) of peer rows I need
+
+    @property
+    def goff(self) -> int:
+        return self.r0 - self.cmin
+
+    @property
+    def n_local(self) -> int:
+        return self.r1 - self.r0
+
+    @property
+    def n_ext(self) -> int:
+        return self.cmax - self.cmin + 1
+
+
+def local_part(a: CsrMatrix, ranges, rank: int) -> LocalPart:
+    r0, r1 = ranges[rank]
+    rp = a.row_ptr[r0:r1 + 1] - a.row_ptr[r0]
+    cols = a.col_idx[a.row_ptr[r0]:a.row_ptr[r1]]
+    vals = a.values[a.row_ptr[r0]:a.row_ptr[r1]]
+    cmin = int(min(cols.min(), r0)) if len(cols) else r0
+    cmax = int(max(cols.max(), r1 - 1)) if len(cols) else r1 - 1
+    csr = CsrMatrix(r1 - r0, cmax - cmin + 1, rp.astype(np.int64), (cols - cmin).astype(np.int64), vals.copy())
+    # interior rows: all columns inside [r0, r1)
+    rows = np.repeat(np.arange(r1 - r0), np.diff(rp))
+    outside = (cols < r0) | (cols >= r1)
+    bad = np.zeros(r1 - r0, bool)
+    bad[rows[outside]] = True
+    good = np.flatnonzero(~bad)
+    # largest contiguous interior block (stencils: everything but one plane on each side)
+    if len(good):
+        runs = np.split(good, np.flatnonzero(np.diff(good) != 1) + 1)
+        best = max(runs, key=len)
+        interior = (int(best[0]), int(best[-1]) + 1)
+    else:
+        interior = (0, 0)
+    part = LocalPart(rank, len(ranges), r0, r1, cmin, cmax, csr, interior)
+    return part
+
+
+def exchange_schedule(parts_bounds: list[tuple[int, int, int, int]], rank: int):
+    """parts_bounds[k] = (r0, r1, cmin, cmax) of every rank -> (sends, recvs) of `rank`."""
+    r0, r1, cmin, cmax = parts_bounds[rank]
+    sends, recvs = {}, {}
+    for peer, (p0, p1, pmin, pmax) in enumerate(parts_bounds):
+        if peer == rank:
+            continue
+        lo, hi = max(p0, cmin), min(p1, cmax + 1)  # peer rows I need
+        if lo < hi:
+            recvs[peer] = (lo, hi)
+        lo, hi = max(r0, pmin), min(r1, pmax + 1)  # my rows the peer needs
+        if lo < hi:
+            sends[peer] = (lo, hi)
+    return sends, recvs
+
+
+class DistributedFilter:
+    """clenshaw_apply over a row partition: Y_local = rho(l(A)) X restricted to my rows.
+
+    ``backend`` provides: alloc(n_rows, q) -> block, rows(block, lo, hi) -> view,
+    copy_rows(dst, src), step(part, mode, g, vin, yin, out, wout, rows, s0..s3),
+    scale(dst, src, s), exchange(ops) and synchronize().
+    """
+
+    def __init__(self, a_global: CsrMatrix, backend, rank: int, world: int, ranges=None):
+        self.world, self.rank = world, rank
+        self.ranges = ranges or partition_rows(a_global, world)
+        self.part = local_part(a_global, self.ranges, rank)
+        bounds = []
+        for k in range(world):
+            p0, p1 = self.ranges[k]
+            cols = a_global.col_idx[a_global.row_ptr[p0]:a_global.row_ptr[p1]]
+            bounds.append((p0, p1, int(min(cols.min(), p0)) if len(cols) else p0,
+                           int(max(cols.max(), p1 - 1)) if len(cols) else p1 - 1))
+        self.part.sends, self.part.recvs = exchange_schedule(bounds, rank)
+        self.backend = backend
+        self.op = backend.upload(self.part)
+
+    # rows of the halo-extended layout
+    def _ext(self, glo, ghi):
+        return glo - self.part.cmin, ghi - self.part.cmin
+
+    def _halo(self, buf):
+        ops = []
+        for peer, (lo, hi) in self.part.sends.items():
+            a, b = self._ext(lo, hi)
+            ops.append(("send", peer, self.backend.rows(buf, a, b)))
+        for peer, (lo, hi) in self.part.recvs.items():
+            a, b = self._ext(lo, hi)
+            ops.append(("recv", peer, self.backend.rows(buf, a, b)))
+        return ops
+
+    def _run(self, mode, g, vin, yin, out, wout, s):
+        """One degree step: exchange g's halo while interior rows compute, then the boundary."""
+        part, be = self.part, self.backend
+        pending = be.exchange_start(self._halo(g)) if part.sends or part.recvs else None
+        i0, i1 = part.interior
+        if i1 > i0:
+            be.step(self.op, part, mode, g, vin, yin, out, wout, (i0, i1), *s)
+        if pending is not None:
+            be.exchange_wait(pending)
+        for lo, hi in ((0, i0), (i1, part.n_local)):
+            if hi > lo:
+                be.step(self.op, part, mode, g, vin, yin, out, wout, (lo, hi), *s)
+
+    def apply(self, coeffs, l1, l2, x_local, degree: int):
+        """x_local: my n_local x q rows (backend block). Returns my rows of rho(l(A)) X."""
+        be, part = self.backend, self.part
+        deg = int(degree)
+        while deg > 0 and coeffs[deg] == 0.0:  # cheb_filter.cpp:141-142
+            deg -= 1
+        q = be.width(x_local)
+        if deg == 0:
+            return be.scale(x_local, float(coeffs[0]))
+        n_ext = part.n_ext
+        a_buf, b_buf = be.alloc(n_ext, q), be.alloc(n_ext, q)
+        g0, g1 = part.goff, part.goff + part.n_local
+        if deg == 1:
+            be.copy_rows(be.rows(a_buf, g0, g1), x_local)
+            out = be.alloc(part.n_local, q)
+            self._run(DEG1, a_buf, None, None, out, None, (coeffs[0], coeffs[1], l1, l2))
+            return out
+        # the First step gathers Y: Y needs its halo too, so stage it in an extended buffer
+        y_ext = be.alloc(n_ext, q)
+        be.copy_rows(be.rows(y_ext, g0, g1), x_local)
+        # w = c_d y -> a_buf ; v -> b_buf
+        self._run(FIRST, y_ext, None, None, be.rows(b_buf, g0, g1), be.rows(a_buf, g0, g1),
+                  (2.0 * l1, 2.0 * l2 + coeffs[deg - 1] / coeffs[deg], coeffs[deg], 0.0))
+        cur_w, cur_v = b_buf, a_buf
+        for j in range(deg - 2, 0, -1):
+            v_rows = be.rows(cur_v, g0, g1)
+            self._run(STEP, cur_w, v_rows, x_local, v_rows, None, (2.0 * l1, 2.0 * l2, coeffs[j], 0.0))
+            cur_w, cur_v = cur_v, cur_w
+        out = be.alloc(part.n_local, q)
+        self._run(STEP, cur_w, be.rows(cur_v, g0, g1), x_local, out, None, (l1, l2, coeffs[0], 0.0))
+        return out
+
+
+class CudaStepBackend:
+    """Device backend: torch CUDA tensors + adp_step_device; halo via torch.distributed (NCCL)."""
+
+    def __init__(self, ctx=None):
+        import torch
+
+        from .operator import default_context
+
+        self.torch = torch
+        self.ctx = ctx or default_context(torch.cuda.current_device())
+
+    def upload(self, part: LocalPart):
+        from .operator import DeviceCsr
+
+        return DeviceCsr(part.csr, self.ctx)
+
+    def alloc(self, n, q):
+        ld = ((q + 1) // 2) * 2
+        return self.torch.zeros(n, ld, dtype=self.torch.float64, device="cuda")[:, :q]
+
+    def width(self, x):
+        return x.shape[1]
+
+    def rows(self, buf, lo, hi):
+        return buf[lo:hi]
+
+    def copy_rows(self, dst, src):
+        dst.copy_(src)
+
+    def scale(self, x, s):
+        return x * s
+
+    def step(self, op, part, mode, g, vin, yin, out, wout, rows, s0, s1, s2, s3):
+        import ctypes as C
+
+        from ._native import check, lib
+
+        t = self.torch
+        self.ctx.set_stream(t.cuda.current_stream())
+        lo, hi = rows
+        ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else C.c_void_p(0)  # noqa: E731
+        q = g.shape[1]
+        ld_y = yin.stride(0) if yin is not None else g.stride(0)
+        ld_out = out.stride(0)
+        check(lib().adp_step_device(self.ctx.h, op.h, mode, ptr(g), g.stride(0), ptr(vin), ptr(yin), ld_y,
+                                    ptr(out), ptr(wout), ld_out, q, lo, hi, part.goff, s0, s1, s2, s3))
+
+    def exchange_start(self, ops):
+        import torch.distributed as dist
+
+        p2p, landing = [], []
+        for kind, peer, buf in ops:
+            if kind == "send":
+                p2p.append(dist.P2POp(dist.isend, buf.contiguous(), peer))
+            else:  # NCCL needs contiguous receive buffers: land, then scatter into the strided rows
+                tmp = buf if buf.is_contiguous() else self.torch.empty(buf.shape, dtype=buf.dtype, device=buf.device)
+                p2p.append(dist.P2POp(dist.irecv, tmp, peer))
+                if tmp is not buf:
+                    landing.append((buf, tmp))
+        return dist.batch_isend_irecv(p2p), landing
+
+    def exchange_wait(self, pending):
+        works, landing = pending
+        for w in works:
+            w.wait()
+        for view, tmp in landing:
+            view.copy_(tmp)
+
+    def synchronize(self):
+        self.torch.cuda.synchronize()

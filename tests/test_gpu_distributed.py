@@ -1,0 +1,106 @@
+"""Row-partitioned filter on the GPU, ranks emulated as threads on ONE device.
+
+Each emulated rank runs DistributedFilter with the CUDA step backend (the
+product kernel, adp_step_device) on its own context and stream; halo rows move
+through a host-side mailbox (the only change versus the NCCL exchange). No
+kernel ever waits on another rank's kernel (B200_PROFILING.md forbids that on
+one GPU): the exchange is host-synchronised. The gathered result must be
+bitwise equal to the single-GPU clenshaw_apply.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2604_00914_b200 as adp
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+class Mailbox:
+    def __init__(self):
+        self.cv = threading.Condition()
+        self.msgs = {}
+
+    def post(self, key, value):
+        with self.cv:
+            self.msgs[key] = value
+            self.cv.notify_all()
+
+    def take(self, key):
+        with self.cv:
+            while key not in self.msgs:
+                self.cv.wait(timeout=60)
+            return self.msgs.pop(key)
+
+
+def make_backend(mailbox, rank):
+    from paper_2604_00914_b200.distributed import CudaStepBackend
+
+    class ThreadBackend(CudaStepBackend):
+        def __init__(self):
+            super().__init__(adp.Context(0))
+            self.calls = 0
+            self.stream = torch.cuda.Stream()
+
+        def exchange_start(self, ops):
+            self.calls += 1
+            torch.cuda.current_stream().synchronize()
+            for kind, peer, buf in ops:
+                if kind == "send":
+                    mailbox.post((rank, peer, self.calls), buf.clone())
+            torch.cuda.synchronize()
+            return [(buf, (peer, rank, self.calls)) for kind, peer, buf in ops if kind == "recv"]
+
+        def exchange_wait(self, pending):
+            for buf, key in pending:
+                buf.copy_(mailbox.take(key))
+
+    return ThreadBackend()
+
+
+def run_ranks(a, world, fn):
+    mailbox = Mailbox()
+    results, errors = [None] * world, []
+
+    def body(rank):
+        try:
+            be = make_backend(mailbox, rank)
+            with torch.cuda.stream(be.stream):
+                results[rank] = fn(rank, be)
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    if errors:
+        raise errors[0]
+    return results
+
+
+@pytest.mark.parametrize("world,degree,q", [(2, 12, 64), (3, 7, 6), (2, 1, 130), (4, 20, 256)])
+def test_emulated_ranks_bitwise(orc, world, degree, q):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_00914_b200 import configs
+    from paper_2604_00914_b200.distributed import DistributedFilter
+
+    a = configs.laplacian7_potential(20, -2.0, 2.0, seed=1)
+    n = a.n_rows
+    f = adp.build_filter(5.9, 6.1, (-2.0, 14.0), 40, 0.5)
+    x = orc.fill_gaussian(n, q, 3, 0)
+    want = adp.clenshaw_apply(f, adp.DeviceCsr(a), x, degree)
+
+    def fn(rank, be):
+        df = DistributedFilter(a, be, rank, world)
+        r0, r1 = df.ranges[rank]
+        xl = torch.from_numpy(np.ascontiguousarray(x[r0:r1])).cuda()
+        return df.apply(f.coeffs, f.l1, f.l2, xl, degree).cpu().numpy()
+
+    got = np.concatenate(run_ranks(a, world, fn))
+    assert np.array_equal(got, want)
