@@ -233,7 +233,7 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
 
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
   return guarded([&] {
-    if (variant < 0 || (variant > 7 && variant < 11) || variant > 15)
+    if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) || variant > 24)
       fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
     ctx->pipe_variant = variant > 10 ? variant - 10 : 0;

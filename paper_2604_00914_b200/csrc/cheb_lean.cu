@@ -259,11 +259,182 @@ void launch_lean(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
   ctx->launches += 1;
 }
 
+// ---- row-block union kernel -----------------------------------------------------------
+// A warp owns R consecutive rows of one panel and walks the UNION of their
+// column sets in ascending order: every distinct W row panel is gathered once
+// and fed to each of the R rows that contain it (the reference's column
+// segments of a row block, tiled_matrix.hpp:78-91, done in registers). Each
+// row still sees its own entries in ascending column order, so the arithmetic
+// -- and every bit of the result -- is unchanged; the L1/L2 gather traffic
+// drops by the operator's intra-block column overlap (27-point stencil, R = 4:
+// 54 instead of 108 row-panel loads). Each row keeps its current and next
+// (col, val) in registers so the union minimum never waits on a load.
+template <class F, int CH, int R, int MODE, class RP, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) cheb_union_kernel(const LArgs p) {
+  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
+  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
+  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
+  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
+  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
+  constexpr int kWarps = kThreads / 32;
+  constexpr uint32_t kPB = 32 * CH * 16u;
+  constexpr int kNone = 0x7fffffff;
+  using Val = typename F::Val;
+  extern __shared__ __align__(16) uint8_t smem[];  // [8 mbarriers][warp][row][V, Y] panels
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int32_t nrows = static_cast<int32_t>(p.nrows);
+  const int32_t nblk = (nrows + R - 1) / R;
+  const int32_t task = static_cast<int32_t>(blockIdx.x) * kWarps + warp;
+  if (task >= nblk * static_cast<int32_t>(p.n_panels)) return;
+  const int32_t panel = task / nblk;
+  const int32_t b = task - panel * nblk;
+  const int64_t r0 = p.row_begin + static_cast<int64_t>(b) * R;
+  const int rows = min(R, nrows - b * R);
+  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
+  const uint32_t voff = poff + lane * 16u;
+  const uint64_t pol = policy_evict_first(1.0f);
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
+  double2* my = reinterpret_cast<double2*>(smem + 128) + warp * (R * 2 * 32 * CH);
+  if constexpr (kStep) {
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      mbar_arrive_expect_tx(bar, 2 * kPB * rows);
+    }
+    __syncwarp();
+    if (lane < rows) {
+      bulk_g2s_hint(my + lane * (2 * 32 * CH), p.vin + static_cast<uint64_t>(r0 + lane) * p.ldg_b + poff, kPB, bar, pol);
+      bulk_g2s_hint(my + lane * (2 * 32 * CH) + 32 * CH, p.yin + static_cast<uint64_t>(r0 + lane) * p.ldy_b + poff, kPB,
+                    bar, pol);
+    }
+  }
+  const char* gb = p.g + voff;
+
+  RP k[R], e[R];
+  int c0[R], c1[R];
+  Val v0[R], v1[R];
+  double2 acc[R][CH];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    k[i] = 0;
+    e[i] = 0;
+    if (i < rows) {
+      k[i] = static_cast<RP>(ld_rp<RP>(p.row_ptr, r0 + i));
+      e[i] = static_cast<RP>(ld_rp<RP>(p.row_ptr, r0 + i + 1));
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if constexpr (kSpmmAcc)
+        acc[i][c] = i < rows ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r0 + i) * p.ldo_b + voff + 512 * c)
+                             : make_double2(0.0, 0.0);
+      else
+        acc[i][c] = make_double2(0.0, 0.0);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    c0[i] = k[i] < e[i] ? __ldg(p.col + k[i]) : kNone;
+    v0[i] = k[i] < e[i] ? F::load(p.val, k[i]) : Val{};
+    c1[i] = k[i] + 1 < e[i] ? __ldg(p.col + k[i] + 1) : kNone;
+    v1[i] = k[i] + 1 < e[i] ? F::load(p.val, k[i] + 1) : Val{};
+  }
+  while (true) {
+    int cmin = c0[0];
+#pragma unroll
+    for (int i = 1; i < R; ++i) cmin = min(cmin, c0[i]);
+    if (cmin == kNone) break;
+    double2 w[CH];
+    const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cmin)) * p.ldg_b);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      w[c] = __ldg(src + 32 * c);
+      if constexpr (kFirst) w[c] = scale2(p.s2, w[c]);
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (c0[i] == cmin) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) acc[i][c] = F::mac(acc[i][c], v0[i], w[c]);
+        ++k[i];
+        c0[i] = c1[i];
+        v0[i] = v1[i];
+        c1[i] = k[i] + 1 < e[i] ? __ldg(p.col + k[i] + 1) : kNone;
+        v1[i] = k[i] + 1 < e[i] ? F::load(p.val, k[i] + 1) : Val{};
+      }
+    }
+  }
+  if constexpr (kStep) {
+    __syncwarp();
+    mbar_wait(bar, 0);
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    if (i >= rows) break;
+    const int64_t r = r0 + i;
+    const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
+    char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      double2 own = make_double2(0.0, 0.0);
+      if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
+      double2 res;
+      if constexpr (kStep) {
+        const double2 vv = my[i * (2 * 32 * CH) + c * 32 + lane];
+        const double2 yy = my[i * (2 * 32 * CH) + 32 * CH + c * 32 + lane];
+        res = add2(sub2(add2(scale2(p.s0, acc[i][c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
+      } else if constexpr (kFirst) {
+        const double2 wn = scale2(p.s2, own);
+        st_hint(p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c, wn, pol);
+        res = add2(scale2(p.s0, acc[i][c]), scale2(p.s1, wn));
+      } else if constexpr (kDeg1) {
+        res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[i][c]), scale2(p.s3, own))));
+      } else {
+        res = acc[i][c];
+      }
+      st_hint(ob + 512 * c, res, pol);
+    }
+  }
+}
+
+template <class F, int CH, int R, class RP, int MINB>
+void launch_union(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
+  constexpr int kWarps = kThreads / 32;
+  k.n_panels = qv / (32 * CH);
+  const int64_t nblk = (k.nrows + R - 1) / R;
+  const int64_t total = nblk * k.n_panels;
+  if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_union: too many tasks");
+  const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
+  const size_t smem = mode == StepMode::Step ? 128 + static_cast<size_t>(kWarps) * R * 2 * 32 * CH * 16 : 16;
+  auto run = [&](auto kern) {
+    if (smem > 48 * 1024)
+      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, kThreads, smem, ctx->stream>>>(k);
+  };
+  switch (mode) {
+    case StepMode::First: run(cheb_union_kernel<F, CH, R, 0, RP, MINB>); break;
+    case StepMode::Step: run(cheb_union_kernel<F, CH, R, 1, RP, MINB>); break;
+    case StepMode::Deg1: run(cheb_union_kernel<F, CH, R, 2, RP, MINB>); break;
+    case StepMode::Spmm: run(cheb_union_kernel<F, CH, R, 3, RP, MINB>); break;
+    case StepMode::SpmmAcc: run(cheb_union_kernel<F, CH, R, 4, RP, MINB>); break;
+  }
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
+}
+
 // Full-panel launch for qv vectors (qv a multiple of the chosen panel). Geometry
 // measured on configs 1-2 (tools/tune_step.py): widest panel with one gathered
 // row in flight per group and many resident warps.
 template <class F, class RP>
 void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_t cap) {
+  switch (ctx->variant) {  // row-block union kernel (tuning variants 21-24)
+    case 21: if (qv % 64 == 0) return launch_union<F, 2, 4, RP, 3>(ctx, mode, k, qv); break;
+    case 22: if (qv % 128 == 0) return launch_union<F, 4, 2, RP, 2>(ctx, mode, k, qv); break;
+    case 23: if (qv % 64 == 0) return launch_union<F, 2, 2, RP, 4>(ctx, mode, k, qv); break;
+    case 24: if (qv % 32 == 0) return launch_union<F, 1, 4, RP, 4>(ctx, mode, k, qv); break;
+    default: break;
+  }
   if (qv % 128 == 0 && cap >= 128) return launch_lean<F, 32, 4, 1, RP, 4>(ctx, mode, k, qv);
   if (qv % 64 == 0 && cap >= 64) return launch_lean<F, 32, 2, 1, RP, 6>(ctx, mode, k, qv);
   if (qv % 32 == 0 && cap >= 32) return launch_lean<F, 32, 1, 1, RP, 8>(ctx, mode, k, qv);

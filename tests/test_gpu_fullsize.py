@@ -1,0 +1,82 @@
+"""Full-size parity on BASELINE.json's configurations 2, 3 and 4 (GPU).
+
+The oracle cannot run a full n x q block at these sizes in seconds, but the
+step kernel computes every column independently: so the GPU result of the
+FULL-width block at full n is checked, column pair by column pair, bitwise
+against the CPU oracle run on just those two columns at full n. Plus the
+size-independent properties: bitwise repeatability, and host-API (column-major,
+pinned) == device-API results.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2604_00914_b200 as adp
+from paper_2604_00914_b200 import _native, configs
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = adp.Context(0)
+    yield c
+    c.close()
+
+
+def device_block(ctx, n, q, complex_=False, seed=3):
+    """Rademacher entries generated on the device (exact: identical to the host Philox fill)."""
+    dt = torch.complex128 if complex_ else torch.float64
+    x = torch.empty(n, q, dtype=dt, device="cuda")
+    if complex_:
+        re = torch.empty(n, q, dtype=torch.float64, device="cuda")
+        im = torch.empty(n, q, dtype=torch.float64, device="cuda")
+        for t, s in ((re, seed), (im, seed + 1)):
+            _native.check(_native.lib().adp_fill_rademacher_device(ctx.h, C.c_void_p(t.data_ptr()), n, q, q, s, 2))
+        x = torch.complex(re, im)
+    else:
+        _native.check(_native.lib().adp_fill_rademacher_device(ctx.h, C.c_void_p(x.data_ptr()), n, q, q, seed, 2))
+    torch.cuda.synchronize()
+    return x
+
+
+@pytest.mark.parametrize("name,degree,cols", [("c2", 8, [(0, 2), (130, 132), (254, 256)]),
+                                              ("c3", 6, [(0, 2), (383, 384)]),
+                                              ("c4", 4, [(0, 2), (1022, 1024)])])
+def test_full_size_columns_bitwise_vs_oracle(ctx, orc, name, degree, cols):
+    cfg = configs.CONFIGS[name]
+    a = cfg.operator()
+    n, q = a.n_rows, cfg.q
+    da = adp.DeviceCsr(a, ctx)
+    k_max = max(degree, 40)
+    f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, k_max, 0.5)
+    g = orc.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, k_max, 0.5)
+    x = device_block(ctx, n, q, a.is_complex)
+    y = adp.clenshaw_apply_device(f, da, x, degree)
+    y2 = adp.clenshaw_apply_device(f, da, x, degree)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)  # bitwise repeatable
+    oa = orc.Csr(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)
+    t = orc.Tiled(oa, 256, 64)
+    for c0, c1 in cols:
+        xs = np.asfortranarray(x[:, c0:c1].cpu().numpy())
+        want = orc.clenshaw_apply(g, t, xs, degree)
+        got = y[:, c0:c1].cpu().numpy()
+        assert np.array_equal(got, want), (name, c0, c1)
+    del y, y2, x
+    torch.cuda.empty_cache()
+
+
+def test_host_api_equals_device_api_config2(ctx):
+    cfg = configs.CONFIGS["c2"]
+    a = cfg.operator()
+    da = adp.DeviceCsr(a, ctx)
+    f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, 40, 0.5)
+    x = device_block(ctx, a.n_rows, 64)
+    yd = adp.clenshaw_apply_device(f, da, x, 5).cpu().numpy()
+    yh = adp.clenshaw_apply(f, da, np.asfortranarray(x.cpu().numpy()), 5)
+    assert np.array_equal(yd, yh)
