@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -233,7 +234,7 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
 
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
   return guarded([&] {
-    if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) || variant > 24)
+    if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) || (variant > 24 && variant < 31) || variant > 33)
       fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
     ctx->pipe_variant = variant > 10 ? variant - 10 : 0;
@@ -280,7 +281,10 @@ adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const in
     a->n_cols = n_cols;
     a->nnz = nnz;
     a->dtype = dtype;
-    a->rp64 = nnz > std::numeric_limits<int32_t>::max();
+    // int64 row offsets when nnz >= 2^31 (config 5); ADP_FORCE_RP64=1 selects them for any size so
+    // the 64-bit path is testable on small operators (tests/test_gpu_parity.py).
+    const char* force64 = std::getenv("ADP_FORCE_RP64");
+    a->rp64 = nnz > std::numeric_limits<int32_t>::max() || (force64 && force64[0] == '1');
     const size_t eb = dtype == ADP_C128 ? 16 : 8;
     try {
       const size_t rp_bytes = (n_rows + 1) * (a->rp64 ? 8 : 4);

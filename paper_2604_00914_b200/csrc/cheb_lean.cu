@@ -433,6 +433,10 @@ void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_
     case 22: if (qv % 128 == 0) return launch_union<F, 4, 2, RP, 2>(ctx, mode, k, qv); break;
     case 23: if (qv % 64 == 0) return launch_union<F, 2, 2, RP, 4>(ctx, mode, k, qv); break;
     case 24: if (qv % 32 == 0) return launch_union<F, 1, 4, RP, 4>(ctx, mode, k, qv); break;
+    // deeper gather batches for long rows (tuning variants 31-33)
+    case 31: if (qv % 32 == 0) return launch_lean<F, 32, 1, 8, RP, 4>(ctx, mode, k, qv); break;
+    case 32: if (qv % 64 == 0) return launch_lean<F, 32, 2, 4, RP, 3>(ctx, mode, k, qv); break;
+    case 33: if (qv % 128 == 0) return launch_lean<F, 32, 4, 4, RP, 2>(ctx, mode, k, qv); break;
     default: break;
   }
   if (qv % 128 == 0 && cap >= 128) return launch_lean<F, 32, 4, 1, RP, 4>(ctx, mode, k, qv);

@@ -231,6 +231,25 @@ def test_complex_bitwise_vs_oracle(ctx, orc):
             assert_bitwise(adp.clenshaw_apply(f, da, x, d), orc.clenshaw_apply(g, t, x, d))
 
 
+def test_int64_row_offsets_path(ctx, orc, monkeypatch):
+    # config 5 (nnz > 2^31) needs int64 row offsets; force them on small operators, real and complex
+    monkeypatch.setenv("ADP_FORCE_RP64", "1")
+    a = orc.random_symmetric(300, 0.03, 17)
+    f, g = same_filter(orc, -0.5, 0.5, (-8.0, 8.0), 30)
+    t = orc.Tiled(a, 256, 64)
+    da = dev(ctx, a)
+    for q in (3, 64, 130):
+        x = orc.fill_gaussian(300, q, q, 1)
+        for d in (1, 2, 30):
+            assert_bitwise(adp.clenshaw_apply(f, da, x, d), orc.clenshaw_apply(g, t, x, d))
+        assert_bitwise(adp.maspmm(da, x), orc.maspmm(t, x))
+    h = random_hermitian(120, 0.05, 3)
+    oh = orc.Csr(h.n_rows, h.n_cols, h.row_ptr, h.col_idx, h.values)
+    xz = np.asfortranarray(np.random.default_rng(1).standard_normal((120, 33)) + 0j)
+    assert_bitwise(adp.clenshaw_apply(f, adp.DeviceCsr(h, ctx), xz, 30),
+                   orc.clenshaw_apply(g, orc.Tiled(oh, 256, 64), xz, 30))
+
+
 # ------------------------------------------------------- full-size configs ---
 def test_config1_full_size_bitwise(ctx, orc):
     from paper_2604_00914_b200 import configs
