@@ -91,6 +91,23 @@ struct Tiling {
 };
 }  // namespace adp
 
+namespace adp {
+// Column-segment layout of R-row blocks (segments.cpp): the reference's
+// TiledMatrix (tiled_matrix.hpp:23-94) with T_i = R -- per row block, the
+// ascending DISTINCT columns its rows touch, a bitmask of the rows that hold
+// each one, and the R values (0 where absent). Used by cheb_seg_kernel.
+struct Segments {
+  int rows_per_block = 0;
+  int64_t n_blocks = 0, n_segs = 0;
+  void* d_blk_ptr = nullptr;  // int64[n_blocks+1]
+  void* d_col = nullptr;      // int32[n_segs]
+  void* d_mask = nullptr;     // uint32[n_segs] (bit i: row i of the block has the column)
+  void* d_val = nullptr;      // Scalar[n_segs * R]
+  double reuse = 0.0;         // nnz / n_segs
+  ~Segments();
+};
+}  // namespace adp
+
 struct adp_csr {
   adp_ctx* ctx = nullptr;
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
@@ -104,6 +121,7 @@ struct adp_csr {
   std::vector<int32_t> h_col;
   void* h_values = nullptr;  // malloc'd copy of the values
   std::vector<std::unique_ptr<adp::Tiling>> tilings;
+  std::vector<std::unique_ptr<adp::Segments>> segments;
 };
 
 namespace adp {
@@ -149,6 +167,9 @@ bool launch_step_tiled(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 bool launch_step_row(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 // The default lean kernel (cheb_lean.cu) for >= 4 vectors per row.
 bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+
+// Column segments of R-row blocks (segments.cpp); built once per (operator, R).
+const Segments* get_segments(adp_csr* a, int rows_per_block);
 
 // Host filter helpers (filter_host.cpp).
 std::vector<double> step_coeffs(double alpha, double beta, int k);

@@ -234,7 +234,10 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
 
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
   return guarded([&] {
-    if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) || (variant > 24 && variant < 31) || variant > 33)
+    // 0 auto; 1-7 one-row kernel; 11-15 pipelined row kernel; 21-24 union; 31-33 deep batches; 41-46 segments
+    if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) ||
+        (variant > 24 && variant < 31) || (variant > 33 && variant < 41) || (variant > 46 && variant < 51) ||
+        variant > 56)
       fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
     ctx->pipe_variant = variant > 10 ? variant - 10 : 0;

@@ -423,11 +423,323 @@ void launch_union(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
   ctx->launches += 1;
 }
 
+// ---- lean kernel with lane-parallel metadata ----------------------------------------------
+// As cheb_lean_kernel (G = 32), but the row's (col, val) window is fetched with
+// one coalesced load (lane k holds entry k) and broadcast by shuffles, so the W
+// gathers depend on no memory load and U of them are issued back to back --
+// removes the per-nonzero (col load -> W load) latency chain of long rows
+// (27-point stencil, config 4).
+template <class F, int CH, int U, int MODE, class RP, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) cheb_lean2_kernel(const LArgs p) {
+  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
+  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
+  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
+  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
+  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
+  constexpr int kWarps = kThreads / 32;
+  constexpr uint32_t kPB = 32 * CH * 16u;
+  using Val = typename F::Val;
+  extern __shared__ __align__(16) uint8_t smem[];
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int32_t nrows = static_cast<int32_t>(p.nrows);
+  int32_t task = static_cast<int32_t>(blockIdx.x) * kWarps + warp;
+  const bool live = task < nrows * static_cast<int32_t>(p.n_panels);
+  if (!live) task = 0;  // no early return: keeps the warp provably converged at the shuffles
+  const int32_t panel = task / nrows;
+  const int64_t r = p.row_begin + (task - panel * nrows);
+  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
+  const uint32_t voff = poff + lane * 16u;
+  const uint64_t pol = policy_evict_first(1.0f);
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
+  double2* my = reinterpret_cast<double2*>(smem + 128) + warp * (2 * 32 * CH);
+  if constexpr (kStep) {
+    if (lane == 0 && live) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      mbar_arrive_expect_tx(bar, 2 * kPB);
+      bulk_g2s_hint(my, p.vin + static_cast<uint64_t>(r) * p.ldg_b + poff, kPB, bar, pol);
+      bulk_g2s_hint(my + 32 * CH, p.yin + static_cast<uint64_t>(r) * p.ldy_b + poff, kPB, bar, pol);
+    }
+  }
+  char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
+  const char* gb = p.g + voff;
+  double2 acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    if constexpr (kSpmmAcc)
+      acc[c] = live ? *reinterpret_cast<const double2*>(ob + 512 * c) : make_double2(0.0, 0.0);
+    else
+      acc[c] = make_double2(0.0, 0.0);
+  }
+  const int64_t start = ld_rp<RP>(p.row_ptr, r);
+  const int cnt_all = live ? static_cast<int>(ld_rp<RP>(p.row_ptr, r + 1) - start) : 0;
+  for (int base = 0; base < cnt_all; base += 32) {
+    const int cnt = min(32, cnt_all - base);
+    int mc = 0;
+    Val mv{};
+    if (lane < cnt) {
+      mc = __ldg(p.col + start + base + lane);
+      mv = F::load(p.val, start + base + lane);
+    }
+    for (int k0 = 0; k0 < cnt; k0 += U) {
+      double2 w[U][CH];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int cidx = __shfl_sync(0xffffffffu, mc, (k0 + u) & 31);
+        if (k0 + u < cnt) {
+          const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
+#pragma unroll
+          for (int c = 0; c < CH; ++c) w[u][c] = __ldg(src + 32 * c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        Val v;
+        if constexpr (std::is_same<Val, double>::value) {
+          v = __shfl_sync(0xffffffffu, mv, (k0 + u) & 31);
+        } else {
+          v.x = __shfl_sync(0xffffffffu, mv.x, (k0 + u) & 31);
+          v.y = __shfl_sync(0xffffffffu, mv.y, (k0 + u) & 31);
+        }
+        if (k0 + u < cnt) {
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            double2 wv = w[u][c];
+            if constexpr (kFirst) wv = scale2(p.s2, wv);
+            acc[c] = F::mac(acc[c], v, wv);
+          }
+        }
+      }
+    }
+  }
+  if (!live) return;
+  if constexpr (kStep) mbar_wait(bar, 0);
+  const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
+  char* wb = kFirst ? p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff : nullptr;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    double2 own = make_double2(0.0, 0.0);
+    if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
+    double2 res;
+    if constexpr (kStep) {
+      const double2 vv = my[c * 32 + lane];
+      const double2 yy = my[32 * CH + c * 32 + lane];
+      res = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
+    } else if constexpr (kFirst) {
+      const double2 wn = scale2(p.s2, own);
+      st_hint(wb + 512 * c, wn, pol);
+      res = add2(scale2(p.s0, acc[c]), scale2(p.s1, wn));
+    } else if constexpr (kDeg1) {
+      res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own))));
+    } else {
+      res = acc[c];
+    }
+    st_hint(ob + 512 * c, res, pol);
+  }
+}
+
+template <class F, int CH, int U, class RP, int MINB>
+void launch_lean2(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
+  constexpr int kWarps = kThreads / 32;
+  k.n_panels = qv / (32 * CH);
+  const int64_t total = k.nrows * k.n_panels;
+  if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_lean2: too many tasks");
+  const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
+  const size_t smem = mode == StepMode::Step ? 128 + static_cast<size_t>(kWarps) * 2 * 32 * CH * 16 : 16;
+  auto run = [&](auto kern) {
+    if (smem > 48 * 1024)
+      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, kThreads, smem, ctx->stream>>>(k);
+  };
+  switch (mode) {
+    case StepMode::First: run(cheb_lean2_kernel<F, CH, U, 0, RP, MINB>); break;
+    case StepMode::Step: run(cheb_lean2_kernel<F, CH, U, 1, RP, MINB>); break;
+    case StepMode::Deg1: run(cheb_lean2_kernel<F, CH, U, 2, RP, MINB>); break;
+    case StepMode::Spmm: run(cheb_lean2_kernel<F, CH, U, 3, RP, MINB>); break;
+    case StepMode::SpmmAcc: run(cheb_lean2_kernel<F, CH, U, 4, RP, MINB>); break;
+  }
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
+}
+
+// ---- column-segment kernel (MaSpMM row blocks) ------------------------------------------
+// A warp owns an R-row block of one panel and walks the block's precomputed
+// distinct columns (segments.cpp): each W row panel is loaded ONCE and applied,
+// from registers, to every row of the block whose bit is set in the segment's
+// mask. Unlike the union kernel the walk has no loop-carried dependency (the
+// segment list is data), so U segments are loaded ahead. Per row the products
+// still accumulate in ascending column order: bitwise the reference's.
+struct SArgs {
+  LArgs l;
+  const int64_t* blk_ptr;
+  const int32_t* seg_col;
+  const uint32_t* seg_mask;
+  const void* seg_val;
+};
+
+template <class F, int CH, int R, int U, int MODE, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) cheb_seg_kernel(const SArgs sa) {
+  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
+  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
+  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
+  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
+  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
+  constexpr int kWarps = kThreads / 32;
+  constexpr uint32_t kPB = 32 * CH * 16u;
+  using Val = typename F::Val;
+  const LArgs& p = sa.l;
+  extern __shared__ __align__(16) uint8_t smem[];  // [8 mbarriers][warp][row][V, Y] panels
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int32_t nrows = static_cast<int32_t>(p.nrows);
+  const int32_t nblk = (nrows + R - 1) / R;
+  const int32_t task = static_cast<int32_t>(blockIdx.x) * kWarps + warp;
+  if (task >= nblk * static_cast<int32_t>(p.n_panels)) return;
+  const int32_t panel = task / nblk;
+  const int32_t b = task - panel * nblk;
+  const int64_t r0 = static_cast<int64_t>(b) * R;  // segments cover the whole operator (row_begin == 0)
+  const int rows = min(R, nrows - b * R);
+  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
+  const uint32_t voff = poff + lane * 16u;
+  const uint64_t pol = policy_evict_first(1.0f);
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
+  double2* my = reinterpret_cast<double2*>(smem + 128) + warp * (R * 2 * 32 * CH);
+  if constexpr (kStep) {
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      mbar_arrive_expect_tx(bar, 2 * kPB * rows);
+    }
+    __syncwarp();
+    if (lane < rows) {
+      bulk_g2s_hint(my + lane * (2 * 32 * CH), p.vin + static_cast<uint64_t>(r0 + lane) * p.ldg_b + poff, kPB, bar, pol);
+      bulk_g2s_hint(my + lane * (2 * 32 * CH) + 32 * CH, p.yin + static_cast<uint64_t>(r0 + lane) * p.ldy_b + poff, kPB,
+                    bar, pol);
+    }
+  }
+  const char* gb = p.g + voff;
+  double2 acc[R][CH];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if constexpr (kSpmmAcc)
+        acc[i][c] = i < rows ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r0 + i) * p.ldo_b + voff + 512 * c)
+                             : make_double2(0.0, 0.0);
+      else
+        acc[i][c] = make_double2(0.0, 0.0);
+    }
+  const int64_t s0 = __ldg(sa.blk_ptr + b), s1 = __ldg(sa.blk_ptr + b + 1);
+  for (int64_t s = s0; s < s1; s += U) {
+    int col[U];
+    uint32_t msk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      col[u] = 0;
+      msk[u] = 0;
+      if (s + u < s1) {
+        col[u] = __ldg(sa.seg_col + s + u);
+        msk[u] = __ldg(sa.seg_mask + s + u);
+      }
+    }
+    double2 w[U][CH];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (s + u < s1) {
+        const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(col[u])) * p.ldg_b);
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          w[u][c] = __ldg(src + 32 * c);
+          if constexpr (kFirst) w[u][c] = scale2(p.s2, w[u][c]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        if ((msk[u] >> i) & 1u) {
+          const Val v = F::load(sa.seg_val, (s + u) * R + i);
+#pragma unroll
+          for (int c = 0; c < CH; ++c) acc[i][c] = F::mac(acc[i][c], v, w[u][c]);
+        }
+      }
+    }
+  }
+  if constexpr (kStep) {
+    __syncwarp();
+    mbar_wait(bar, 0);
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    if (i >= rows) break;
+    const int64_t r = r0 + i;
+    const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
+    char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      double2 own = make_double2(0.0, 0.0);
+      if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
+      double2 res;
+      if constexpr (kStep) {
+        const double2 vv = my[i * (2 * 32 * CH) + c * 32 + lane];
+        const double2 yy = my[i * (2 * 32 * CH) + 32 * CH + c * 32 + lane];
+        res = add2(sub2(add2(scale2(p.s0, acc[i][c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
+      } else if constexpr (kFirst) {
+        const double2 wn = scale2(p.s2, own);
+        st_hint(p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c, wn, pol);
+        res = add2(scale2(p.s0, acc[i][c]), scale2(p.s1, wn));
+      } else if constexpr (kDeg1) {
+        res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[i][c]), scale2(p.s3, own))));
+      } else {
+        res = acc[i][c];
+      }
+      st_hint(ob + 512 * c, res, pol);
+    }
+  }
+}
+
+template <class F, int CH, int R, int U, int MINB>
+bool launch_seg(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, const adp_csr* a) {
+  if (k.row_begin != 0 || k.nrows != a->n_rows) return false;  // segments cover whole operators
+  const Segments* sg = get_segments(const_cast<adp_csr*>(a), R);
+  constexpr int kWarps = kThreads / 32;
+  SArgs sa{};
+  sa.l = k;
+  sa.l.n_panels = qv / (32 * CH);
+  sa.blk_ptr = static_cast<const int64_t*>(sg->d_blk_ptr);
+  sa.seg_col = static_cast<const int32_t*>(sg->d_col);
+  sa.seg_mask = static_cast<const uint32_t*>(sg->d_mask);
+  sa.seg_val = sg->d_val;
+  const int64_t total = sg->n_blocks * sa.l.n_panels;
+  if (total >= (int64_t{1} << 31)) return false;
+  const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
+  const size_t smem = mode == StepMode::Step ? 128 + static_cast<size_t>(kWarps) * R * 2 * 32 * CH * 16 : 16;
+  auto run = [&](auto kern) {
+    if (smem > 48 * 1024)
+      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, kThreads, smem, ctx->stream>>>(sa);
+  };
+  switch (mode) {
+    case StepMode::First: run(cheb_seg_kernel<F, CH, R, U, 0, MINB>); break;
+    case StepMode::Step: run(cheb_seg_kernel<F, CH, R, U, 1, MINB>); break;
+    case StepMode::Deg1: run(cheb_seg_kernel<F, CH, R, U, 2, MINB>); break;
+    case StepMode::Spmm: run(cheb_seg_kernel<F, CH, R, U, 3, MINB>); break;
+    case StepMode::SpmmAcc: run(cheb_seg_kernel<F, CH, R, U, 4, MINB>); break;
+  }
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
+  return true;
+}
+
 // Full-panel launch for qv vectors (qv a multiple of the chosen panel). Geometry
 // measured on configs 1-2 (tools/tune_step.py): widest panel with one gathered
 // row in flight per group and many resident warps.
 template <class F, class RP>
-void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_t cap) {
+void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_t cap, const adp_csr* a) {
   switch (ctx->variant) {  // row-block union kernel (tuning variants 21-24)
     case 21: if (qv % 64 == 0) return launch_union<F, 2, 4, RP, 3>(ctx, mode, k, qv); break;
     case 22: if (qv % 128 == 0) return launch_union<F, 4, 2, RP, 2>(ctx, mode, k, qv); break;
@@ -437,6 +749,20 @@ void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_
     case 31: if (qv % 32 == 0) return launch_lean<F, 32, 1, 8, RP, 4>(ctx, mode, k, qv); break;
     case 32: if (qv % 64 == 0) return launch_lean<F, 32, 2, 4, RP, 3>(ctx, mode, k, qv); break;
     case 33: if (qv % 128 == 0) return launch_lean<F, 32, 4, 4, RP, 2>(ctx, mode, k, qv); break;
+    // column-segment (MaSpMM row-block) kernel (tuning variants 41-46)
+    case 41: if (qv % 64 == 0 && launch_seg<F, 2, 4, 2, 2>(ctx, mode, k, qv, a)) return; break;
+    case 42: if (qv % 128 == 0 && launch_seg<F, 4, 2, 2, 2>(ctx, mode, k, qv, a)) return; break;
+    case 43: if (qv % 32 == 0 && launch_seg<F, 1, 8, 2, 2>(ctx, mode, k, qv, a)) return; break;
+    case 44: if (qv % 64 == 0 && launch_seg<F, 2, 2, 4, 3>(ctx, mode, k, qv, a)) return; break;
+    case 45: if (qv % 32 == 0 && launch_seg<F, 1, 4, 4, 4>(ctx, mode, k, qv, a)) return; break;
+    case 46: if (qv % 128 == 0 && launch_seg<F, 4, 4, 1, 1>(ctx, mode, k, qv, a)) return; break;
+    // lane-parallel metadata (tuning variants 51-56)
+    case 51: if (qv % 128 == 0) return launch_lean2<F, 4, 2, RP, 2>(ctx, mode, k, qv); break;
+    case 52: if (qv % 128 == 0) return launch_lean2<F, 4, 4, RP, 2>(ctx, mode, k, qv); break;
+    case 53: if (qv % 64 == 0) return launch_lean2<F, 2, 4, RP, 3>(ctx, mode, k, qv); break;
+    case 54: if (qv % 64 == 0) return launch_lean2<F, 2, 8, RP, 2>(ctx, mode, k, qv); break;
+    case 55: if (qv % 32 == 0) return launch_lean2<F, 1, 8, RP, 4>(ctx, mode, k, qv); break;
+    case 56: if (qv % 128 == 0) return launch_lean2<F, 4, 1, RP, 4>(ctx, mode, k, qv); break;
     default: break;
   }
   if (qv % 128 == 0 && cap >= 128) return launch_lean<F, 32, 4, 1, RP, 4>(ctx, mode, k, qv);
@@ -501,11 +827,11 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
     kk.out += off;
     kk.wout = k.wout ? k.wout + off : nullptr;
     if (cplx) {
-      if (a->rp64) launch_full<CplxL, int64_t>(ctx, mode, kk, take, cap);
-      else launch_full<CplxL, int32_t>(ctx, mode, kk, take, cap);
+      if (a->rp64) launch_full<CplxL, int64_t>(ctx, mode, kk, take, cap, a);
+      else launch_full<CplxL, int32_t>(ctx, mode, kk, take, cap, a);
     } else {
-      if (a->rp64) launch_full<RealL, int64_t>(ctx, mode, kk, take, cap);
-      else launch_full<RealL, int32_t>(ctx, mode, kk, take, cap);
+      if (a->rp64) launch_full<RealL, int64_t>(ctx, mode, kk, take, cap, a);
+      else launch_full<RealL, int32_t>(ctx, mode, kk, take, cap, a);
     }
     done += take;
   }
