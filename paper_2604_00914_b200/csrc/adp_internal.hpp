@@ -68,6 +68,7 @@ struct adp_ctx {
   int pipe_variant = 0;  // derived: variant - 10 for the pipelined row kernel
   // tile kernel knobs (0 = default): chunks per lane, pipeline stages, stage KiB, CTAs per SM
   int tile_ch = 0, tile_stages = 0, tile_stage_kb = 0, tile_ctas = 0;
+  int pair_variant = 0;  // two-step (pair) kernel geometry; 0 = off
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;
   void* cusolver = nullptr;
@@ -108,6 +109,19 @@ struct Segments {
 };
 }  // namespace adp
 
+namespace adp {
+// Chunk dependency plan of an operator for the two-step pair kernel (cheb_pair.cu).
+struct PairPlan {
+  int64_t chunk_rows = 0, gs = 0, nch = 0, ngroups = 0, reach = 0;
+  void* d_glo = nullptr;       // int32[nch]: first counter group a step-(j-1) chunk waits on
+  void* d_ghi = nullptr;       // int32[nch]: last one
+  void* d_counters = nullptr;  // uint32[counter_panels * ngroups], cumulative completion counts
+  int64_t counter_panels = 0;
+  uint32_t epoch = 0;
+  ~PairPlan();
+};
+}  // namespace adp
+
 struct adp_csr {
   adp_ctx* ctx = nullptr;
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
@@ -122,6 +136,7 @@ struct adp_csr {
   void* h_values = nullptr;  // malloc'd copy of the values
   std::vector<std::unique_ptr<adp::Tiling>> tilings;
   std::vector<std::unique_ptr<adp::Segments>> segments;
+  std::vector<std::unique_ptr<adp::PairPlan>> pair_plans;
 };
 
 namespace adp {
@@ -167,6 +182,22 @@ bool launch_step_tiled(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 bool launch_step_row(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 // The default lean kernel (cheb_lean.cu) for >= 4 vectors per row.
 bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+
+// Two consecutive in-place Clenshaw steps in one launch (cheb_pair.cu): step j
+// reads g (gathered), v, y and writes v; step j-1 gathers that v, reads g and y
+// and writes out (== g in place, or the final output). Returns false when the
+// pair kernel is off or does not apply; the caller then runs two single steps.
+struct PairStep {
+  const void* g;
+  void* v;
+  const void* y;
+  void* out;
+  int64_t ld, ld_y, ld_out;  // elements
+  double f0, f1, f2;         // step j scalars
+  double b0, b1, b2;         // step j-1 scalars
+};
+bool launch_pair(adp_ctx* ctx, const adp_csr* a, const PairStep& ps, int64_t q);
+PairPlan* get_pair_plan(adp_csr* a, int64_t chunk_rows, int64_t gs, int64_t n_panels);
 
 // Column segments of R-row blocks (segments.cpp); built once per (operator, R).
 const Segments* get_segments(adp_csr* a, int rows_per_block);

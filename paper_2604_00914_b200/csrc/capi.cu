@@ -99,26 +99,66 @@ void clenshaw_device(adp_ctx* ctx, const adp_csr* a, const double* coeffs, doubl
   s.yin = y;
   s.ld = ld;
   s.ld_y = ld_y;
-  for (int j = deg - 2; j >= 1; --j) {  // v = ((2l1 A w + 2l2 w) - v) + c_j y ; swap
+  // Steps j = deg-2 .. 1: v = ((2l1 A w + 2l2 w) - v) + c_j y ; swap. Step 0 (the
+  // last): v = ((l1 A w + l2 w) - v) + c0 y, written straight to the output.
+  auto scalars = [&](int j, double* t) {
+    t[0] = j == 0 ? l1 : 2.0 * l1;
+    t[1] = j == 0 ? l2 : 2.0 * l2;
+    t[2] = coeffs[j];
+  };
+  int j = deg - 2;
+  // With the pair kernel (cheb_pair.cu) steps run two per launch; an odd count
+  // runs its first step alone.
+  if (ctx->pair_variant != 0 && (j + 1) % 2 == 1 && j >= 1) {
     s.gsrc = cur_w;
     s.vin = cur_v;
     s.out = cur_v;
     s.ld_out = ld;
-    s.s0 = 2.0 * l1;
-    s.s1 = 2.0 * l2;
-    s.s2 = coeffs[j];
+    double t[3];
+    scalars(j, t);
+    s.s0 = t[0];
+    s.s1 = t[1];
+    s.s2 = t[2];
+    launch_step(ctx, StepMode::Step, s);
+    std::swap(cur_w, cur_v);
+    --j;
+  }
+  for (; j >= 0; --j) {
+    if (ctx->pair_variant != 0 && j >= 1) {
+      PairStep ps{};
+      ps.g = cur_w;
+      ps.v = cur_v;
+      ps.y = y;
+      ps.out = j - 1 == 0 ? out : cur_w;
+      ps.ld = ld;
+      ps.ld_y = ld_y;
+      ps.ld_out = j - 1 == 0 ? ld_out : ld;
+      double t[3];
+      scalars(j, t);
+      ps.f0 = t[0];
+      ps.f1 = t[1];
+      ps.f2 = t[2];
+      scalars(j - 1, t);
+      ps.b0 = t[0];
+      ps.b1 = t[1];
+      ps.b2 = t[2];
+      if (launch_pair(ctx, a, ps, q)) {  // b_j in cur_v, b_{j-1} in cur_w (or out)
+        --j;
+        continue;
+      }
+    }
+    s.gsrc = cur_w;
+    s.vin = cur_v;
+    s.out = j == 0 ? out : cur_v;
+    s.ld_out = j == 0 ? ld_out : ld;
+    double t[3];
+    scalars(j, t);
+    s.s0 = t[0];
+    s.s1 = t[1];
+    s.s2 = t[2];
     launch_step(ctx, StepMode::Step, s);
     std::swap(cur_w, cur_v);
   }
-  // v = ((l1 A w + l2 w) - v) + c0 y, written straight to the output
-  s.gsrc = cur_w;
-  s.vin = cur_v;
-  s.out = out;
-  s.ld_out = ld_out;
-  s.s0 = l1;
-  s.s1 = l2;
-  s.s2 = coeffs[0];
-  launch_step(ctx, StepMode::Step, s);
 }
 
 void check_filter_args(const adp_csr* a, const double* coeffs, int32_t k_max, int32_t degree, int64_t x_rows,
@@ -237,10 +277,11 @@ adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
     // 0 auto; 1-7 one-row kernel; 11-15 pipelined row kernel; 21-24 union; 31-33 deep batches; 41-46 segments
     if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) ||
         (variant > 24 && variant < 31) || (variant > 33 && variant < 41) || (variant > 46 && variant < 51) ||
-        variant > 56)
+        (variant > 56 && variant < 61) || (variant > 66 && variant < 71) || variant > 76)
       fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
-    ctx->pipe_variant = variant > 10 ? variant - 10 : 0;
+    ctx->pair_variant = variant > 70 ? variant - 70 : 0;
+    ctx->pipe_variant = (variant > 10 && variant < 16) ? variant - 10 : 0;
   });
 }
 

@@ -48,6 +48,7 @@ struct LArgs {
   char* wout;
   uint32_t ldg_b, ldy_b, ldo_b;  // leading dimensions in bytes
   int64_t row_begin, nrows, n_panels, goff;
+  int64_t g_rows;  // rows of the gathered operand (the operator's column count)
   double s0, s1, s2, s3;
 };
 
@@ -564,6 +565,163 @@ void launch_lean2(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
   ctx->launches += 1;
 }
 
+// ---- row-window kernel ----------------------------------------------------------------------
+// A CTA of WARPS warps owns WARPS consecutive rows (one per warp) of one column
+// panel. The gathered operand's rows [r0 - H, r0 + WARPS + H) -- the band every
+// row of the block touches through its near-diagonal entries (the x-line of a
+// stencil) and its own row -- are bulk-copied ONCE per CTA into shared memory;
+// gathers whose column falls in that window read shared memory, the rest read
+// global memory through L1 as in the lean kernel. Cuts the L2->SM gather
+// traffic of a 7-point stencil from 7 to 4 + (WARPS+2H)/WARPS row panels per row
+// and removes the own-row reload. Accumulation order per row is unchanged (CSR
+// order), so results are bitwise the lean kernel's.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <class F, int CH, int WARPS, int H, int MODE, class RP, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) cheb_win_kernel(const LArgs p) {
+  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
+  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
+  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
+  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
+  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
+  constexpr uint32_t kPB = 32 * CH * 16u;
+  constexpr int kWin = WARPS + 2 * H;
+  using Val = typename F::Val;
+  extern __shared__ __align__(16) uint8_t smem[];  // [2 mbarriers | pad][window rows][warp][V, Y]
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int32_t nrows = static_cast<int32_t>(p.nrows);
+  const int32_t nblk = (nrows + WARPS - 1) / WARPS;
+  const int32_t panel = static_cast<int32_t>(blockIdx.x) / nblk;
+  const int32_t b = static_cast<int32_t>(blockIdx.x) - panel * nblk;
+  const int32_t rows = min(WARPS, nrows - b * WARPS);
+  const int64_t r0 = p.row_begin + static_cast<int64_t>(b) * WARPS;  // first out row of the block
+  const int64_t g0 = r0 + p.goff;                                     // its own row in the gathered operand
+  const int64_t wlo = g0 - H > 0 ? g0 - H : 0;
+  const int64_t whi = g0 + rows + H < p.g_rows ? g0 + rows + H : p.g_rows;
+  const uint32_t wn = static_cast<uint32_t>(whi - wlo);
+  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
+  const uint32_t voff = poff + lane * 16u;
+
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* vbar = wbar + 1;
+  double2* win = reinterpret_cast<double2*>(smem + 128);
+  double2* vy = win + kWin * 32 * CH;
+  if (threadIdx.x == 0) {
+    mbar_init(wbar, 1);
+    mbar_init(vbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    mbar_arrive_expect_tx(wbar, kPB * wn);
+    if constexpr (kStep) mbar_arrive_expect_tx(vbar, 2 * kPB * static_cast<uint32_t>(rows));
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint64_t pol = policy_evict_first(1.0f);
+    for (uint32_t i = lane; i < wn; i += 32)  // WARPS + 2H may exceed 32
+      bulk_g2s(win + i * 32 * CH, p.g + static_cast<uint64_t>(wlo + i) * p.ldg_b + poff, kPB, wbar);
+    if constexpr (kStep) {
+      if (lane < rows) {
+        bulk_g2s_hint(vy + lane * 2 * 32 * CH, p.vin + static_cast<uint64_t>(r0 + lane) * p.ldg_b + poff, kPB, vbar, pol);
+        bulk_g2s_hint(vy + lane * 2 * 32 * CH + 32 * CH, p.yin + static_cast<uint64_t>(r0 + lane) * p.ldy_b + poff, kPB,
+                      vbar, pol);
+      }
+    }
+  }
+  if (warp >= rows) return;
+  const uint64_t pol = policy_evict_first(1.0f);
+  const int64_t r = r0 + warp;
+  char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
+  const char* gb = p.g + voff;
+  double2 acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    if constexpr (kSpmmAcc)
+      acc[c] = *reinterpret_cast<const double2*>(ob + 512 * c);
+    else
+      acc[c] = make_double2(0.0, 0.0);
+  }
+  bool ready = false;
+  const RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r));
+  const RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r + 1));
+  for (RP e = start; e < end; ++e) {
+    const int cidx = __ldg(p.col + e);
+    const Val v = F::load(p.val, static_cast<int64_t>(e));
+    const uint32_t rel = static_cast<uint32_t>(cidx - static_cast<int32_t>(wlo));
+    double2 w[CH];
+    if (rel < wn) {
+      if (!ready) {
+        mbar_wait(wbar, 0);
+        ready = true;
+      }
+#pragma unroll
+      for (int c = 0; c < CH; ++c) w[c] = win[rel * (32 * CH) + c * 32 + lane];
+    } else {
+      const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) w[c] = __ldg(src + 32 * c);
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      double2 wv = w[c];
+      if constexpr (kFirst) wv = scale2(p.s2, wv);
+      acc[c] = F::mac(acc[c], v, wv);
+    }
+  }
+  if (!ready) mbar_wait(wbar, 0);  // also: no CTA exit with bulk copies in flight
+  if constexpr (kStep) mbar_wait(vbar, 0);
+  const uint32_t own_rel = static_cast<uint32_t>(g0 + warp - wlo);
+  char* wb = kFirst ? p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff : nullptr;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    double2 own = make_double2(0.0, 0.0);
+    if constexpr (kNeedOwn) own = win[own_rel * (32 * CH) + c * 32 + lane];
+    double2 res;
+    if constexpr (kStep) {
+      const double2 vv = vy[warp * 2 * 32 * CH + c * 32 + lane];
+      const double2 yy = vy[warp * 2 * 32 * CH + 32 * CH + c * 32 + lane];
+      res = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
+    } else if constexpr (kFirst) {
+      const double2 wn2 = scale2(p.s2, own);
+      st_hint(wb + 512 * c, wn2, pol);
+      res = add2(scale2(p.s0, acc[c]), scale2(p.s1, wn2));
+    } else if constexpr (kDeg1) {
+      res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own))));
+    } else {
+      res = acc[c];
+    }
+    st_hint(ob + 512 * c, res, pol);
+  }
+}
+
+template <class F, int CH, int WARPS, int H, class RP, int MINB>
+void launch_win(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
+  k.n_panels = qv / (32 * CH);
+  const int64_t nblk = (k.nrows + WARPS - 1) / WARPS;
+  const int64_t total = nblk * k.n_panels;
+  if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_win: too many blocks");
+  constexpr size_t kWinBytes = static_cast<size_t>(WARPS + 2 * H) * 32 * CH * 16;
+  const size_t smem = 128 + kWinBytes + (mode == StepMode::Step ? static_cast<size_t>(WARPS) * 2 * 32 * CH * 16 : 0);
+  auto run = [&](auto kern) {
+    if (smem > 48 * 1024)
+      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<static_cast<int>(total), WARPS * 32, smem, ctx->stream>>>(k);
+  };
+  switch (mode) {
+    case StepMode::First: run(cheb_win_kernel<F, CH, WARPS, H, 0, RP, MINB>); break;
+    case StepMode::Step: run(cheb_win_kernel<F, CH, WARPS, H, 1, RP, MINB>); break;
+    case StepMode::Deg1: run(cheb_win_kernel<F, CH, WARPS, H, 2, RP, MINB>); break;
+    case StepMode::Spmm: run(cheb_win_kernel<F, CH, WARPS, H, 3, RP, MINB>); break;
+    case StepMode::SpmmAcc: run(cheb_win_kernel<F, CH, WARPS, H, 4, RP, MINB>); break;
+  }
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
+}
+
 // ---- column-segment kernel (MaSpMM row blocks) ------------------------------------------
 // A warp owns an R-row block of one panel and walks the block's precomputed
 // distinct columns (segments.cpp): each W row panel is loaded ONCE and applied,
@@ -763,6 +921,13 @@ void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_
     case 54: if (qv % 64 == 0) return launch_lean2<F, 2, 8, RP, 2>(ctx, mode, k, qv); break;
     case 55: if (qv % 32 == 0) return launch_lean2<F, 1, 8, RP, 4>(ctx, mode, k, qv); break;
     case 56: if (qv % 128 == 0) return launch_lean2<F, 4, 1, RP, 4>(ctx, mode, k, qv); break;
+    // row-window kernel (tuning variants 61-66)
+    case 61: if (qv % 128 == 0) return launch_win<F, 4, 8, 1, RP, 4>(ctx, mode, k, qv); break;
+    case 62: if (qv % 128 == 0) return launch_win<F, 4, 16, 1, RP, 2>(ctx, mode, k, qv); break;
+    case 63: if (qv % 64 == 0) return launch_win<F, 2, 8, 1, RP, 6>(ctx, mode, k, qv); break;
+    case 64: if (qv % 128 == 0) return launch_win<F, 4, 32, 1, RP, 1>(ctx, mode, k, qv); break;
+    case 65: if (qv % 64 == 0) return launch_win<F, 2, 16, 1, RP, 3>(ctx, mode, k, qv); break;
+    case 66: if (qv % 128 == 0) return launch_win<F, 4, 4, 1, RP, 8>(ctx, mode, k, qv); break;
     default: break;
   }
   if (qv % 128 == 0 && cap >= 128) return launch_lean<F, 32, 4, 1, RP, 4>(ctx, mode, k, qv);
@@ -798,6 +963,7 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   k.row_begin = s.row_begin;
   k.nrows = s.row_end - s.row_begin;
   k.goff = s.goff;
+  k.g_rows = a->n_cols;
   k.s0 = s.s0;
   k.s1 = s.s1;
   k.s2 = s.s2;
