@@ -69,6 +69,8 @@ struct adp_ctx {
   // tile kernel knobs (0 = default): chunks per lane, pipeline stages, stage KiB, CTAs per SM
   int tile_ch = 0, tile_stages = 0, tile_stage_kb = 0, tile_ctas = 0;
   int pair_variant = 0;  // two-step (pair) kernel geometry; 0 = off
+  adp::DevBuf sched;      // task tickets of persistent kernels (self re-arming)
+  bool sched_ready = false;
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;
   void* cusolver = nullptr;
@@ -122,6 +124,19 @@ struct PairPlan {
 };
 }  // namespace adp
 
+namespace adp {
+// Shifted-pattern row blocks of an operator for the line kernel (cheb_line.cu).
+struct LinePlan {
+  int R = 0, mm = 0;
+  int64_t n_blocks = 0, n_regular = 0, n_patterns = 0, n_runs = 0;
+  double regular_frac = 0.0;
+  void* d_blk_pat = nullptr;  // int32[n_blocks]: pattern id, -1 = row by row
+  void* d_pat_ptr = nullptr;  // int32[n_patterns+1]: runs of each pattern
+  void* d_runs = nullptr;     // int4[n_runs]: {first column - r0, entry index, length, 0}
+  ~LinePlan();
+};
+}  // namespace adp
+
 struct adp_csr {
   adp_ctx* ctx = nullptr;
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
@@ -137,6 +152,7 @@ struct adp_csr {
   std::vector<std::unique_ptr<adp::Tiling>> tilings;
   std::vector<std::unique_ptr<adp::Segments>> segments;
   std::vector<std::unique_ptr<adp::PairPlan>> pair_plans;
+  std::vector<std::unique_ptr<adp::LinePlan>> line_plans;
 };
 
 namespace adp {
@@ -198,6 +214,11 @@ struct PairStep {
 };
 bool launch_pair(adp_ctx* ctx, const adp_csr* a, const PairStep& ps, int64_t q);
 PairPlan* get_pair_plan(adp_csr* a, int64_t chunk_rows, int64_t gs, int64_t n_panels);
+
+// The line kernel (cheb_line.cu): register reuse of gathered rows across
+// blocks of rows with shifted column patterns. Returns false if not applicable.
+bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+const LinePlan* get_line_plan(adp_csr* a, int rows_per_block, int max_run);
 
 // Column segments of R-row blocks (segments.cpp); built once per (operator, R).
 const Segments* get_segments(adp_csr* a, int rows_per_block);

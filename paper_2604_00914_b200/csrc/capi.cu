@@ -243,6 +243,7 @@ adp_status adp_ctx_destroy(adp_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     adp_release_dense_handles(ctx);
     for (auto& b : ctx->ws) b.release();
+    ctx->sched.release();
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -277,10 +278,11 @@ adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
     // 0 auto; 1-7 one-row kernel; 11-15 pipelined row kernel; 21-24 union; 31-33 deep batches; 41-46 segments
     if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) ||
         (variant > 24 && variant < 31) || (variant > 33 && variant < 41) || (variant > 46 && variant < 51) ||
-        (variant > 56 && variant < 61) || (variant > 66 && variant < 71) || variant > 76)
+        (variant > 56 && variant < 61) || (variant > 66 && variant < 71) || (variant > 76 && variant < 81) ||
+        variant > 97)
       fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
-    ctx->pair_variant = variant > 70 ? variant - 70 : 0;
+    ctx->pair_variant = (variant > 70 && variant < 77) ? variant - 70 : 0;
     ctx->pipe_variant = (variant > 10 && variant < 16) ? variant - 10 : 0;
   });
 }

@@ -278,3 +278,52 @@ def test_config2_full_size_bitwise_low_degree(ctx, orc):
     got = adp.clenshaw_apply(f, da, x, 4)
     assert_bitwise(got, orc.clenshaw_apply(g, orc.Tiled(oa, 256, 64), x, 4))
     assert np.array_equal(adp.clenshaw_apply(f, da, x, 4), got)
+
+
+# ------------------------------------------------- every kernel variant ---
+# All step kernels (lean, union, deep batch, column segments, lane-parallel
+# metadata, row window, two-step pair, line / pipelined line) must be bitwise
+# equal to the oracle: they only reorganise loads, never the per-element
+# arithmetic. Stencil operators exercise the shifted-pattern blocks (and their
+# irregular faces), a random matrix the row-by-row fallbacks.
+VARIANTS = [0, 1, 11, 21, 22, 31, 33, 41, 42, 51, 56, 61, 62, 64, 71, 72, 73, 81, 82, 83, 84, 86, 88, 91, 92, 94, 97]
+
+
+@pytest.mark.parametrize("kind", ["lap7", "lap27", "random", "hermitian"])
+def test_kernel_variants_bitwise(ctx, orc, kind):
+    from paper_2604_00914_b200 import configs
+
+    if kind == "lap7":
+        a = configs.laplacian7_potential(11, -2.0, 2.0, seed=3)
+    elif kind == "lap27":
+        a = configs.dft_like_27pt(9, n_centres=4, seed=1)
+    elif kind == "random":
+        a = adp.CsrMatrix(*(lambda m: (m.n_rows, m.n_cols, m.row_ptr, m.col_idx, m.values))(orc.random_symmetric(700, 0.01, 5)))
+    else:
+        a = random_hermitian(300, 0.03, 9)
+    n = a.n_rows
+    oa = orc.Csr(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)
+    t = orc.Tiled(oa, 256, 64)
+    dense_bounds = (-30.0, 30.0)
+    f, g = same_filter(orc, -0.3, 0.4, dense_bounds, 12)
+    da = adp.DeviceCsr(a, ctx)
+    rng = np.random.default_rng(n)
+    for q in (64, 256):
+        x = rng.standard_normal((n, q))
+        if a.is_complex:
+            x = x + 1j * rng.standard_normal((n, q))
+        x = np.asfortranarray(x)
+        want = {d: orc.clenshaw_apply(g, t, x, d) for d in (1, 2, 5, 12)}
+        want_spmm = None if a.is_complex else orc.maspmm(t, x)  # the oracle's maspmm is real-only
+        try:
+            for v in VARIANTS:
+                ctx.set_tuning(v)
+                for d, w in want.items():
+                    try:
+                        assert_bitwise(adp.clenshaw_apply(f, da, x, d), w)
+                    except AssertionError as e:
+                        raise AssertionError(f"variant {v} degree {d} q {q}: {e}") from None
+                if want_spmm is not None:
+                    assert_bitwise(adp.maspmm(da, x), want_spmm)
+        finally:
+            ctx.set_tuning(0)
