@@ -375,7 +375,7 @@ def run_ours(args):
             "pct_of_hbm_peak": round(100.0 * value / world / peak, 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "cheb_lean_kernel (fused Clenshaw step, csrc/cheb_row.cu)",
+                         "kernel": "cheb_lean_kernel (fused Clenshaw step, csrc/cheb_lean.cu)",
                          "peak_source": peak_src,
                          "launch_ms": round(launch_ms, 5)},
             "gpu_launches": launches,

@@ -49,6 +49,7 @@ struct LArgs {
   uint32_t ldg_b, ldy_b, ldo_b;  // leading dimensions in bytes
   int64_t row_begin, nrows, n_panels, goff;
   int64_t g_rows;  // rows of the gathered operand (the operator's column count)
+  int32_t valid;   // masked launches: vectors of the (single) panel that exist
   double s0, s1, s2, s3;
 };
 
@@ -124,7 +125,7 @@ __device__ __forceinline__ int64_t ld_rp(const void* p, int64_t i) {
   return static_cast<int64_t>(__ldg(static_cast<const RP*>(p) + i));
 }
 
-template <class F, int G, int CH, int U, int MODE, class RP, int MINB>
+template <class F, int G, int CH, int U, int MODE, class RP, int MINB, bool MASK = false>
 __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p) {
   constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
   constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
@@ -148,13 +149,18 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + grp;
   double2* my = reinterpret_cast<double2*>(smem + ((kGroups * 8 + 15) / 16) * 16) + grp * (2 * G * CH);
+  // masked launches (ragged widths): one panel whose vectors >= p.valid do not exist
+  bool ok[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) ok[c] = !MASK || c * G + lane < p.valid;
+  const uint32_t cpb = MASK ? static_cast<uint32_t>(p.valid) * 16u : kPB;  // bytes of the panel that exist
   if constexpr (kStep) {
     if (lane == 0) {
       mbar_init(bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      mbar_arrive_expect_tx(bar, 2 * kPB);
-      bulk_g2s_hint(my, p.vin + static_cast<uint64_t>(r) * p.ldg_b + poff, kPB, bar, pol);
-      bulk_g2s_hint(my + G * CH, p.yin + static_cast<uint64_t>(r) * p.ldy_b + poff, kPB, bar, pol);
+      mbar_arrive_expect_tx(bar, 2 * cpb);
+      bulk_g2s_hint(my, p.vin + static_cast<uint64_t>(r) * p.ldg_b + poff, cpb, bar, pol);
+      bulk_g2s_hint(my + G * CH, p.yin + static_cast<uint64_t>(r) * p.ldy_b + poff, cpb, bar, pol);
     }
   }
   char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
@@ -164,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     if constexpr (kSpmmAcc)
-      acc[c] = *reinterpret_cast<const double2*>(ob + G * 16 * c);
+      acc[c] = ok[c] ? *reinterpret_cast<const double2*>(ob + G * 16 * c) : make_double2(0.0, 0.0);
     else
       acc[c] = make_double2(0.0, 0.0);
   }
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
         const double2* src =
             reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx[u])) * p.ldg_b);
 #pragma unroll
-        for (int c = 0; c < CH; ++c) w[u][c] = __ldg(src + G * c);
+        for (int c = 0; c < CH; ++c) w[u][c] = ok[c] ? __ldg(src + G * c) : make_double2(0.0, 0.0);
       }
     }
 #pragma unroll
@@ -211,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
   char* wb = kFirst ? p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff : nullptr;
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
+    if (!ok[c]) continue;
     double2 own = make_double2(0.0, 0.0);
     if constexpr (kNeedOwn) own = __ldg(own_src + G * c);
     double2 res;
@@ -234,10 +241,11 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
   }
 }
 
-template <class F, int G, int CH, int U, class RP, int MINB>
+template <class F, int G, int CH, int U, class RP, int MINB, bool MASK = false>
 void launch_lean(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
   constexpr int kGroups = kThreads / G;
-  k.n_panels = qv / (G * CH);
+  k.n_panels = MASK ? 1 : qv / (G * CH);
+  k.valid = static_cast<int32_t>(qv);
   const int64_t total = k.nrows * k.n_panels;
   if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_lean: too many tasks");
   const int grid = static_cast<int>((total + kGroups - 1) / kGroups);
@@ -250,11 +258,11 @@ void launch_lean(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
     kern<<<grid, kThreads, smem, ctx->stream>>>(k);
   };
   switch (mode) {
-    case StepMode::First: run(cheb_lean_kernel<F, G, CH, U, 0, RP, MINB>); break;
-    case StepMode::Step: run(cheb_lean_kernel<F, G, CH, U, 1, RP, MINB>); break;
-    case StepMode::Deg1: run(cheb_lean_kernel<F, G, CH, U, 2, RP, MINB>); break;
-    case StepMode::Spmm: run(cheb_lean_kernel<F, G, CH, U, 3, RP, MINB>); break;
-    case StepMode::SpmmAcc: run(cheb_lean_kernel<F, G, CH, U, 4, RP, MINB>); break;
+    case StepMode::First: run(cheb_lean_kernel<F, G, CH, U, 0, RP, MINB, MASK>); break;
+    case StepMode::Step: run(cheb_lean_kernel<F, G, CH, U, 1, RP, MINB, MASK>); break;
+    case StepMode::Deg1: run(cheb_lean_kernel<F, G, CH, U, 2, RP, MINB, MASK>); break;
+    case StepMode::Spmm: run(cheb_lean_kernel<F, G, CH, U, 3, RP, MINB, MASK>); break;
+    case StepMode::SpmmAcc: run(cheb_lean_kernel<F, G, CH, U, 4, RP, MINB, MASK>); break;
   }
   ADP_LAUNCH_CHECK();
   ctx->launches += 1;
@@ -938,6 +946,30 @@ void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_
   return launch_lean<F, 4, 1, 1, RP, 8>(ctx, mode, k, qv);  // qv % 4 == 0
 }
 
+
+// Masked geometry for a ragged tail of 5..127 vectors: quarter-warp groups up
+// to 16 vectors, half-warp groups (two rows per warp in flight) up to 64,
+// whole warps beyond (c1s solver widths: tools/tune_step.py --q).
+template <class F, class RP>
+void launch_masked_t(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t rem) {
+  if (rem <= 16) return launch_lean<F, 8, 2, 1, RP, 8, true>(ctx, mode, k, rem);
+  if (rem <= 32) return launch_lean<F, 16, 2, 1, RP, 6, true>(ctx, mode, k, rem);
+  if (rem <= 48) return launch_lean<F, 16, 3, 1, RP, 4, true>(ctx, mode, k, rem);
+  if (rem <= 64) return launch_lean<F, 16, 4, 1, RP, 4, true>(ctx, mode, k, rem);
+  if (rem <= 96) return launch_lean<F, 32, 3, 1, RP, 4, true>(ctx, mode, k, rem);
+  return launch_lean<F, 32, 4, 1, RP, 4, true>(ctx, mode, k, rem);
+}
+
+void launch_masked(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t rem, bool cplx, bool rp64) {
+  if (cplx) {
+    if (rp64) launch_masked_t<CplxL, int64_t>(ctx, mode, k, rem);
+    else launch_masked_t<CplxL, int32_t>(ctx, mode, k, rem);
+  } else {
+    if (rp64) launch_masked_t<RealL, int64_t>(ctx, mode, k, rem);
+    else launch_masked_t<RealL, int32_t>(ctx, mode, k, rem);
+  }
+}
+
 }  // namespace
 
 bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
@@ -977,6 +1009,21 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   while (qv - done >= 4) {
     const int64_t rem = qv - done;
     int64_t take;
+    const bool one_piece = rem == 4 || rem == 8 || rem == 16 || rem == 32 || rem == 64 || rem == 96;
+    if (rem < 128 && rem > 4 && !one_piece && ctx->variant == 0 && cap >= 128) {
+      // ragged tail of 5..127 vectors: ONE masked launch (a split into
+      // power-of-two panels re-reads the operator and pays a launch per piece)
+      LArgs kk = k;
+      const uint32_t off = static_cast<uint32_t>(done * 16);
+      kk.g += off;
+      kk.vin = k.vin ? k.vin + off : nullptr;
+      kk.yin = k.yin ? k.yin + off : nullptr;
+      kk.out += off;
+      kk.wout = k.wout ? k.wout + off : nullptr;
+      launch_masked(ctx, mode, kk, rem, cplx, a->rp64);
+      done = qv;
+      break;
+    }
     if (rem >= 128 && cap >= 128) take = (rem / 128) * 128;
     else if (rem >= 64 && cap >= 64) take = (rem / 64) * 64;
     else if (rem >= 32 && cap >= 32) take = (rem / 32) * 32;
