@@ -73,7 +73,14 @@ adp_status adp_ctx_synchronize(adp_ctx* ctx);
 int64_t adp_ctx_launch_count(const adp_ctx* ctx);
 /* Kernel tuning knobs (0 = automatic): columns per warp task (panel width). */
 adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
-/* Kernel tuning variant of the fused step kernel (0 = automatic). */
+/* Kernel tuning variant of the fused step kernel (0 = automatic; see DESIGN.md
+ * 3.1c). Every variant computes bit-identical results; they differ only in how
+ * the gathered rows travel: 1-7 one-row-per-group kernel, 11-15 pipelined row
+ * kernel, 21-24 row-block union, 31-33 deeper gather batches, 41-46 column
+ * segments, 51-56 lane-parallel metadata, 61-66 shared-memory row window,
+ * 71-76 two degree steps per launch, 81-91 line kernel (register reuse across
+ * shifted-pattern row blocks), 92-97 line kernel with a TMA ring. Other values
+ * fail with ADP_ERR_CONFIG. */
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant);
 /* Tile-kernel knobs (0 = default): 16-byte vectors per lane per panel (1-4),
  * shared-memory pipeline stages, KiB per stage, resident CTAs per SM. */

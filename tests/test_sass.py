@@ -53,6 +53,11 @@ def test_tma_and_async_copies_present(sass):
     assert lean_step and all(any("UBLKCP" in ln for ln in funcs[f]) for f in lean_step)
     row_step = [f for f in funcs if "cheb_row_kernel" in f and re.search(r"ELi1E[il]Li\dELb", f)]
     assert row_step and all(any("LDGSTS" in ln for ln in funcs[f]) for f in row_step)
+    # the pipelined line kernel moves every gathered run as a 2-D tensor-map tile (UTMALDG)
+    linep = [f for f in funcs if "cheb_linep_kernel" in f]
+    assert linep and all(any("UTMALDG" in ln for ln in funcs[f]) for f in linep)
+    pair = [f for f in funcs if "cheb_pair_kernel" in f]
+    assert pair and all(any("UBLKCP" in ln for ln in funcs[f]) for f in pair)
 
 
 def test_no_odd_uniform_descriptors(sass):
@@ -65,7 +70,10 @@ def test_no_odd_uniform_descriptors(sass):
 
 def test_step_kernels_have_no_fma(sass):
     _, funcs = sass
-    step = [f for f in funcs if re.search(r"cheb_(step|row|lean|tile)_kernel", f)]
+    step = [f for f in funcs if re.search(r"cheb_\w+_kernel", f)]
+    # every fused-step design: lean, lean2, union, seg, win, pair, line, linep, row, tile, step
+    for name in ("cheb_lean_kernel", "cheb_pair_kernel", "cheb_line_kernel", "cheb_linep_kernel", "cheb_win_kernel"):
+        assert any(name in f for f in step), name
     assert step
     fused = [f for f in step if any(re.search(r"\bDFMA\b", ln) for ln in funcs[f])]
     assert not fused, fused[:3]
