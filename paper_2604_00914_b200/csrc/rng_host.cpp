@@ -2,9 +2,12 @@
 // (initial basis, trace probes, Lanczos start, top-up) and of the synthetic
 // configuration generators. Restates proj/include/adapoly/philox.hpp:18-109 so
 // seeded blocks are bit-identical to the reference's.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <numbers>
+#include <thread>
+#include <vector>
 
 #include "adp_internal.hpp"
 
@@ -55,22 +58,65 @@ struct Philox {
   }
 };
 
+// Draw i depends on i alone (counter-based), so blocks of the index range can be
+// filled by independent threads with bit-identical results; chunks start on
+// multiples of 4 so each Philox block is computed once.
+template <class Fn>
+void parallel_range(int64_t total, Fn fn) {
+  const int64_t kMin = int64_t{1} << 16;
+  const int64_t hw = std::max<int64_t>(1, std::min<int64_t>(32, std::thread::hardware_concurrency()));
+  const int64_t nt = std::min<int64_t>(hw, (total + kMin - 1) / kMin);
+  if (nt <= 1) {
+    fn(int64_t{0}, total);
+    return;
+  }
+  const int64_t chunk = ((total + nt - 1) / nt + 3) / 4 * 4;
+  std::vector<std::thread> th;
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t b = t * chunk, e = std::min(total, b + chunk);
+    if (b < e) th.emplace_back(fn, b, e);
+  }
+  for (auto& x : th) x.join();
+}
+
 }  // namespace
 
 extern "C" {
 
+// Column-major n x q block: element (r, c) is draw c * n + r (philox.hpp:96-98),
+// i.e. draw i lands at out[i].
 adp_status adp_fill_gaussian(double* out, int64_t n, int64_t q, uint64_t seed, uint64_t stream) {
   const Philox rng(seed, stream);
-  for (int64_t c = 0; c < q; ++c)
-    for (int64_t r = 0; r < n; ++r) out[c * n + r] = rng.gaussian(static_cast<uint64_t>(c * n + r));
+  parallel_range(n * q, [&](int64_t b, int64_t e) {
+    int64_t i = b;
+    while (i < e) {
+      uint32_t w[4];
+      rng.block(static_cast<uint64_t>(i) / 4, w);
+      for (int64_t j = i; j < std::min(e, (i / 4 + 1) * 4); ++j) {
+        const unsigned pair = static_cast<unsigned>((j % 4) / 2);
+        const double u1 = (static_cast<double>(w[2 * pair]) + 0.5) * 0x1p-32;
+        const double u2 = (static_cast<double>(w[2 * pair + 1]) + 0.5) * 0x1p-32;
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        const double t = 2.0 * std::numbers::pi * u2;
+        out[j] = (j % 2 == 0) ? r * std::cos(t) : r * std::sin(t);
+      }
+      i = (i / 4 + 1) * 4;
+    }
+  });
   return ADP_OK;
 }
 
 adp_status adp_fill_rademacher(double* out, int64_t n, int64_t q, uint64_t seed, uint64_t stream) {
   const Philox rng(seed, stream);
-  for (int64_t c = 0; c < q; ++c)
-    for (int64_t r = 0; r < n; ++r)
-      out[c * n + r] = (rng.word(static_cast<uint64_t>(c * n + r)) >> 31) != 0 ? 1.0 : -1.0;
+  parallel_range(n * q, [&](int64_t b, int64_t e) {
+    int64_t i = b;
+    while (i < e) {
+      uint32_t w[4];
+      rng.block(static_cast<uint64_t>(i) / 4, w);
+      for (int64_t j = i; j < std::min(e, (i / 4 + 1) * 4); ++j) out[j] = (w[j % 4] >> 31) != 0 ? 1.0 : -1.0;
+      i = (i / 4 + 1) * 4;
+    }
+  });
   return ADP_OK;
 }
 
