@@ -70,6 +70,7 @@ struct adp_ctx {
   int tile_ch = 0, tile_stages = 0, tile_stage_kb = 0, tile_ctas = 0;
   int pair_variant = 0;  // two-step (pair) kernel geometry; 0 = off
   adp::DevBuf sched;      // task tickets of persistent kernels (self re-arming)
+  bool pdl = true;        // programmatic dependent launch between degree steps (ADP_NO_PDL=1: off)
   bool sched_ready = false;
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;
@@ -156,6 +157,24 @@ struct adp_csr {
 };
 
 namespace adp {
+
+// Launch with programmatic stream serialization (PDL) when the context allows
+// it: the kernel must execute griddepcontrol.wait before reading anything the
+// previous kernel on the stream writes.
+template <class Kern, class Args>
+void launch_pdl(adp_ctx* ctx, Kern kern, dim3 grid, dim3 block, size_t smem, const Args& args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ADP_CUDA(cudaLaunchKernelEx(&cfg, kern, args));
+}
 
 // ---- kernels (cheb_step.cu) ---------------------------------------------------
 enum class StepMode : int { First = 0, Step = 1, Deg1 = 2, Spmm = 3, SpmmAcc = 4 };

@@ -230,6 +230,8 @@ adp_status adp_ctx_create(int32_t device, adp_ctx** out) {
       throw;
     }
     ctx->stream = ctx->own_stream;
+    const char* no_pdl = std::getenv("ADP_NO_PDL");
+    ctx->pdl = !(no_pdl && no_pdl[0] == '1');
     *out = ctx;
   });
 }

@@ -124,6 +124,15 @@ template <class RP>
 __device__ __forceinline__ int64_t ld_rp(const void* p, int64_t i) {
   return static_cast<int64_t>(__ldg(static_cast<const RP*>(p) + i));
 }
+// Programmatic dependent launch: consecutive degree steps are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so this grid's CTAs can be
+// resident while the previous step drains; nothing the previous step writes is
+// read before griddepcontrol.wait (a no-op for ordinary launches). The next
+// step may start launching as soon as every CTA of this one got here.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
 
 template <class F, int G, int CH, int U, int MODE, class RP, int MINB, bool MASK = false>
 __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p) {
@@ -149,6 +158,9 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + grp;
   double2* my = reinterpret_cast<double2*>(smem + ((kGroups * 8 + 15) / 16) * 16) + grp * (2 * G * CH);
+  const RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r));  // the operator is constant: before the wait
+  const RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r + 1));
+  pdl_wait_and_release();
   // masked launches (ragged widths): one panel whose vectors >= p.valid do not exist
   bool ok[CH];
 #pragma unroll
@@ -174,8 +186,6 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
     else
       acc[c] = make_double2(0.0, 0.0);
   }
-  const RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r));
-  const RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r + 1));
   for (RP e = start; e < end; e += U) {
     int cidx[U];
     Val v[U];
@@ -255,7 +265,7 @@ void launch_lean(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
   auto run = [&](auto kern) {
     if (smem > 48 * 1024)
       ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, kThreads, smem, ctx->stream>>>(k);
+    launch_pdl(ctx, kern, dim3(grid), dim3(kThreads), smem, k);
   };
   switch (mode) {
     case StepMode::First: run(cheb_lean_kernel<F, G, CH, U, 0, RP, MINB, MASK>); break;

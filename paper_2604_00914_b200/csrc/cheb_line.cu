@@ -253,6 +253,9 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
   double2* my = reinterpret_cast<double2*>(smem + 128) + warp * (R * 2 * 32 * CH);
+  const int32_t pid = __ldg(p.blk_pat + b);  // operator data: before the wait
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");  // see pdl_wait_and_release (cheb_lean.cu)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if constexpr (kStep) {
     if (lane == 0) {
       mbar_init(bar, 1);
@@ -278,7 +281,6 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
       else
         acc[i][c] = make_double2(0.0, 0.0);
     }
-  const int32_t pid = __ldg(p.blk_pat + b);
   if (pid >= 0) {  // shifted-pattern block: R full rows
     int64_t rs[R];
 #pragma unroll
@@ -408,7 +410,7 @@ bool launch_line_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
   auto run = [&](auto kern) {
     if (smem > 48 * 1024)
       ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, kThreads, smem, ctx->stream>>>(k);
+    launch_pdl(ctx, kern, dim3(grid), dim3(kThreads), smem, k);
   };
   switch (mode) {
     case StepMode::First: run(cheb_line_kernel<F, CH, R, MM, 0, RP, MINB, UNR>); break;
