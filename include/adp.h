@@ -157,6 +157,20 @@ adp_status adp_initial_degree(double alpha, double beta, double c, int32_t* out)
 adp_status adp_adaptive_degree(const adp_filter_info* f, const double* coeffs, const double* ritz, int64_t p,
                                int64_t e_i, double tau_a, int32_t* out);
 
+/* ------------------------------------------------------- filter bounds -- */
+/* Truncation-error diagnostics of the damped step filter
+ * (include/adapoly/filter_bounds.hpp:8-30, src/filter_bounds.cpp): J(theta),
+ * the damping constant C_m (m > 0, else ADP_ERR_CONFIG), the pointwise
+ * undamped (k >= 1) and damped (1 <= k_i <= k, m >= 0) bounds on |g - g_k|,
+ * and the projector bound ||P - P_i||_2 from the eigenvalue angles
+ * (non-empty, 1 <= k_i <= k_max). */
+adp_status adp_j_theta(double theta, double alpha, double beta, double* out);
+adp_status adp_c_m_constant(double m, double* out);
+adp_status adp_undamped_bound(double theta, int32_t k, double alpha, double beta, double* out);
+adp_status adp_damped_bound(double theta, int32_t k_i, int32_t k, double m, double alpha, double beta, double* out);
+adp_status adp_projector_bound(const adp_filter_info* f, const double* thetas, int64_t count, int32_t k_i,
+                               double* out);
+
 /* ------------------------------------------------------------- seeded RNG -- */
 /* fill_gaussian / fill_rademacher (include/adapoly/philox.hpp:92-109) into a
  * host column-major n x q buffer: Philox4x32-10, draw index c*n + r. */

@@ -6,6 +6,8 @@ CPU fallback, and calls raise if the shared library is not built.
 """
 from ._native import (AdpError, CollectiveError, ConfigError, CudaError, DimensionError, NotPositiveDefinite,
                       OutOfMemory, ParseError, lib)
+from .bounds import (c_m_constant, damped_bound, inspect_filter, inspect_filter_csv, j_theta, projector_bound,
+                     undamped_bound)
 from .filter import (ChebFilter, SpectrumBounds, adaptive_degree, build_filter, chebyshev_step_coeffs,
                      eval_filter_scalar, initial_degree, jackson_damping, lanczos_damping)
 from .operator import (Context, DeviceCsr, clenshaw_apply, clenshaw_apply_device, default_context, maspmm,
@@ -17,6 +19,8 @@ from .sparse import (CsrMatrix, fill_gaussian, fill_rademacher, parse_matrix_mar
                      philox_gaussian, philox_uniform, read_matrix_market)
 
 __all__ = [
+    "c_m_constant", "damped_bound", "inspect_filter", "inspect_filter_csv", "j_theta", "projector_bound",
+    "undamped_bound",
     "AdpError", "CollectiveError", "ConfigError", "CudaError", "DimensionError", "NotPositiveDefinite",
     "OutOfMemory", "ParseError", "lib", "ChebFilter", "SpectrumBounds", "adaptive_degree", "build_filter",
     "chebyshev_step_coeffs", "eval_filter_scalar", "initial_degree", "jackson_damping", "lanczos_damping",

@@ -96,6 +96,11 @@ SIGNATURES = {
     "adp_build_filter": (I32, [D, D, D, D, I32, D, I32, P, P]),
     "adp_eval_filter": (I32, [P, P, P, I64, I32, P, P]),
     "adp_initial_degree": (I32, [D, D, D, P]),
+    "adp_j_theta": (I32, [D, D, D, P]),
+    "adp_c_m_constant": (I32, [D, P]),
+    "adp_undamped_bound": (I32, [D, I32, D, D, P]),
+    "adp_damped_bound": (I32, [D, I32, I32, D, D, D, P]),
+    "adp_projector_bound": (I32, [P, P, I64, I32, P]),
     "adp_adaptive_degree": (I32, [P, P, P, I64, I64, D, P]),
     "adp_fill_gaussian": (I32, [P, I64, I64, U64, U64]),
     "adp_fill_rademacher": (I32, [P, I64, I64, U64, U64]),
