@@ -63,6 +63,10 @@ class SolverConfig:
     p_override: int | None = None
     spurious_detection: bool = True
     collect_diagnostics: bool = False
+    # The reference's CPU tiling knobs (solver.hpp:28-29, csr_to_tiled T_i / T_k). The GPU keeps CSR
+    # and does not use them; they are accepted so configs and RunReports round-trip unchanged.
+    tile_ti: int | None = None
+    tile_tk: int | None = None
 
     def to_c(self) -> CSolverConfig:
         return CSolverConfig(self.interval_a, self.interval_b, self.tau_c, self.tau_a, self.m, self.c,

@@ -232,3 +232,27 @@ def test_inspect_filter_sweep():
     for bad in (dict(degree=0), dict(degree=101), dict(bounds=(1.0, -1.0)), dict(samples=-1)):
         with pytest.raises(adp.ConfigError):
             adp.inspect_filter(-0.2, 0.3, **bad)
+
+
+# proj/tests/test_cli.cpp:218-269 (inspect-filter)
+def test_inspect_filter_full_interval_rho_is_one():
+    rows = adp.inspect_filter_csv(-1.0, 1.0, (-1.0, 1.0), k=40, m=0.5, samples=25).splitlines()
+    assert len(rows) == 26 and rows[0] == "x,rho,error,bound"
+    assert all(",1," in r for r in rows[1:])
+
+
+def test_inspect_filter_zero_samples_header_only():
+    assert adp.inspect_filter_csv(0.1, 0.6, samples=0) == "x,rho,error,bound\n"
+
+
+def test_inspect_filter_error_dominated_by_bound():
+    rows = adp.inspect_filter_csv(0.1, 0.6, (-1.0, 1.0), k=100, m=0.5, samples=500, sweep=(-0.1, 0.3)).splitlines()
+    assert len(rows) == 501
+    compared = 0
+    for r in rows[1:]:
+        x, rho, err, bound = (float(v) for v in r.split(","))
+        if abs(x - 0.1) <= 1e-3:
+            continue
+        compared += 1
+        assert err <= bound
+    assert compared >= 490
