@@ -13,6 +13,7 @@ from .filter import (ChebFilter, SpectrumBounds, adaptive_degree, build_filter, 
 from .operator import (Context, DeviceCsr, clenshaw_apply, clenshaw_apply_device, default_context, maspmm,
                        maspmm_device)
 from .report import RunReport, dump_report, run_report_from_json, run_solve, to_json
+from .slicing import SlicedResult, balanced_slices, slice_interval, solve_sliced
 from .solver import (IterationRecord, SolveResult, SolverConfig, StageTimings, cholesky_qr_device,
                      compute_residuals_device, estimate_eigcount, estimate_spectrum_bounds, rayleigh_ritz_device,
                      solve, spurious_threshold)
@@ -20,6 +21,7 @@ from .sparse import (CsrMatrix, fill_gaussian, fill_rademacher, parse_matrix_mar
                      philox_gaussian, philox_uniform, read_matrix_market)
 
 __all__ = [
+    "SlicedResult", "balanced_slices", "slice_interval", "solve_sliced",
     "RunReport", "dump_report", "run_report_from_json", "run_solve", "to_json",
     "c_m_constant", "damped_bound", "inspect_filter", "inspect_filter_csv", "j_theta", "projector_bound",
     "undamped_bound",

@@ -139,7 +139,8 @@ struct LinePlan {
 }  // namespace adp
 
 struct adp_csr {
-  adp_ctx* ctx = nullptr;
+  adp_ctx* ctx = nullptr;     // creating context (must outlive every call that uses this operator)
+  int device = 0;             // destroy needs only this: the operator may outlive its context
   int64_t n_rows = 0, n_cols = 0, nnz = 0;
   adp_dtype dtype = ADP_F64;
   bool rp64 = false;          // int64 row offsets (nnz >= 2^31)

@@ -370,8 +370,7 @@ adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const in
 adp_status adp_csr_destroy(adp_csr* a) {
   return guarded([&] {
     if (!a) return;
-    cudaSetDevice(a->ctx->device);
-    cudaStreamSynchronize(a->ctx->stream);
+    cudaSetDevice(a->device);  // cudaFree waits for work still using the buffers
     cudaFree(a->row_ptr);
     cudaFree(a->col_idx);
     cudaFree(a->values);
