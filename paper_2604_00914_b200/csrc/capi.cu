@@ -325,6 +325,7 @@ adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const in
     set_device(ctx);
     auto* a = new adp_csr;
     a->ctx = ctx;
+    a->device = ctx->device;
     a->n_rows = n_rows;
     a->n_cols = n_cols;
     a->nnz = nnz;
