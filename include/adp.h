@@ -78,7 +78,7 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
  * the gathered rows travel: 1-7 one-row-per-group kernel, 11-15 pipelined row
  * kernel, 21-24 row-block union, 31-33 deeper gather batches, 41-46 column
  * segments, 51-56 lane-parallel metadata, 61-66 shared-memory row window,
- * 71-76 two degree steps per launch, 81-91 line kernel (register reuse across
+ * 71-76 two degree steps per launch, 81-91 and 98 line kernel (register reuse across
  * shifted-pattern row blocks), 92-97 line kernel with a TMA ring. Other values
  * fail with ADP_ERR_CONFIG. */
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant);

@@ -747,6 +747,7 @@ bool dispatch_line(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
     case 89: return launch_line_cfg<F, 2, 4, 3, RP, 1, 2>(ctx, mode, s, qv, 0.0);
     case 90: return launch_line_cfg<F, 1, 4, 3, RP, 2, 2>(ctx, mode, s, qv, 0.0);
     case 91: return launch_line_cfg<F, 2, 2, 3, RP, 4, 1>(ctx, mode, s, qv, 0.0);
+    case 98: return launch_line_cfg<F, 2, 3, 3, RP, 2, 1>(ctx, mode, s, qv, 0.0);
     // pipelined (TMA ring) variants: <CH, R, MM, S, NW, MINB>
     case 92: return launch_linep_cfg<F, 2, 2, 3, 6, 4, RP, 1>(ctx, mode, s, qv);
     case 93: return launch_linep_cfg<F, 2, 4, 3, 3, 4, RP, 1>(ctx, mode, s, qv);
