@@ -71,6 +71,7 @@ struct adp_ctx {
   int pair_variant = 0;  // two-step (pair) kernel geometry; 0 = off
   adp::DevBuf sched;      // task tickets of persistent kernels (self re-arming)
   bool pdl = true;        // programmatic dependent launch between degree steps (ADP_NO_PDL=1: off)
+  bool auto_line = true;  // automatic line-kernel choice (ADP_NO_LINE=1: off, for A/B timing)
   bool sched_ready = false;
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;

@@ -232,6 +232,8 @@ adp_status adp_ctx_create(int32_t device, adp_ctx** out) {
     ctx->stream = ctx->own_stream;
     const char* no_pdl = std::getenv("ADP_NO_PDL");
     ctx->pdl = !(no_pdl && no_pdl[0] == '1');
+    const char* no_line = std::getenv("ADP_NO_LINE");
+    ctx->auto_line = !(no_line && no_line[0] == '1');
     *out = ctx;
   });
 }

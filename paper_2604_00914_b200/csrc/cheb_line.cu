@@ -132,6 +132,7 @@ struct LnArgs {
   char* wout;
   uint32_t ldg_b, ldy_b, ldo_b;
   int32_t nrows, nblk, n_panels;
+  int32_t valid;  // masked launches: vectors of the single panel that exist
   int64_t goff;
   const int32_t* blk_pat;
   const int32_t* pat_ptr;
@@ -227,7 +228,7 @@ __device__ __forceinline__ void tma2d_hint(void* dst, const CUtensorMap* tm, int
       : "memory");
 }
 
-template <class F, int CH, int R, int MM, int MODE, class RP, int MINB, int UNR>
+template <class F, int CH, int R, int MM, int MODE, class RP, int MINB, int UNR, bool MASK>
 __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs p) {
   constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
   constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
@@ -253,6 +254,11 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
   double2* my = reinterpret_cast<double2*>(smem + 128) + warp * (R * 2 * 32 * CH);
+  // masked launches (ragged widths): one panel whose vectors >= p.valid do not exist
+  bool ok[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) ok[c] = !MASK || c * 32 + lane < p.valid;
+  const uint32_t cpb = MASK ? static_cast<uint32_t>(p.valid) * 16u : kPB;
   const int32_t pid = __ldg(p.blk_pat + b);  // operator data: before the wait
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // see pdl_wait_and_release (cheb_lean.cu)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -260,13 +266,13 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
     if (lane == 0) {
       mbar_init(bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      mbar_arrive_expect_tx(bar, 2 * kPB * static_cast<uint32_t>(rows));
+      mbar_arrive_expect_tx(bar, 2 * cpb * static_cast<uint32_t>(rows));
     }
     __syncwarp();
     if (lane < rows) {
       const uint64_t r = static_cast<uint64_t>(r0 + lane);
-      bulk_g2s_hint(my + lane * (2 * 32 * CH), p.vin + r * p.ldg_b + poff, kPB, bar, pol);
-      bulk_g2s_hint(my + lane * (2 * 32 * CH) + 32 * CH, p.yin + r * p.ldy_b + poff, kPB, bar, pol);
+      bulk_g2s_hint(my + lane * (2 * 32 * CH), p.vin + r * p.ldg_b + poff, cpb, bar, pol);
+      bulk_g2s_hint(my + lane * (2 * 32 * CH) + 32 * CH, p.yin + r * p.ldy_b + poff, cpb, bar, pol);
     }
   }
   const char* gb = p.g + voff;
@@ -276,8 +282,9 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       if constexpr (kSpmmAcc)
-        acc[i][c] = i < rows ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r0 + i) * p.ldo_b + voff + 512 * c)
-                             : make_double2(0.0, 0.0);
+        acc[i][c] = (i < rows && ok[c])
+                        ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r0 + i) * p.ldo_b + voff + 512 * c)
+                        : make_double2(0.0, 0.0);
       else
         acc[i][c] = make_double2(0.0, 0.0);
     }
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
           const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(c0 + j) * p.ldg_b);
 #pragma unroll
           for (int c = 0; c < CH; ++c) {
-            w[j][c] = __ldg(src + 32 * c);
+            w[j][c] = ok[c] ? __ldg(src + 32 * c) : make_double2(0.0, 0.0);
             if constexpr (kFirst) w[j][c] = scale2(p.s2, w[j][c]);  // W = c_d * Y on the fly
           }
         }
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
           const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
 #pragma unroll
           for (int c = 0; c < CH; ++c) {
-            double2 wv = __ldg(src + 32 * c);
+            double2 wv = ok[c] ? __ldg(src + 32 * c) : make_double2(0.0, 0.0);
             if constexpr (kFirst) wv = scale2(p.s2, wv);
             acc[i][c] = F::mac(acc[i][c], v, wv);
           }
@@ -347,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
       char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
+        if (!ok[c]) continue;
         double2 own = make_double2(0.0, 0.0);
         if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
         double2 res;
@@ -372,10 +380,10 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
   }
 }
 
-template <class F, int CH, int R, int MM, class RP, int MINB, int UNR = 1>
+template <class F, int CH, int R, int MM, class RP, int MINB, int UNR = 1, bool MASK = false>
 bool launch_line_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv, double min_regular) {
   const adp_csr* a = s.a;
-  if (qv % (32 * CH) != 0) return false;
+  if (MASK ? (qv > 32 * CH || qv <= 32 * (CH - 1)) : qv % (32 * CH) != 0) return false;
   const LinePlan* plan = get_line_plan(const_cast<adp_csr*>(a), R, MM);
   if (plan->regular_frac < min_regular) return false;
   constexpr int kWarps = kThreads / 32;
@@ -394,7 +402,8 @@ bool launch_line_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
   k.ldo_b = static_cast<uint32_t>((s.ld_out / epv) * 16);
   k.nrows = static_cast<int32_t>(a->n_rows);
   k.nblk = static_cast<int32_t>(plan->n_blocks);
-  k.n_panels = static_cast<int32_t>(qv / (32 * CH));
+  k.n_panels = MASK ? 1 : static_cast<int32_t>(qv / (32 * CH));
+  k.valid = static_cast<int32_t>(qv);
   k.goff = s.goff;
   k.blk_pat = static_cast<const int32_t*>(plan->d_blk_pat);
   k.pat_ptr = static_cast<const int32_t*>(plan->d_pat_ptr);
@@ -413,11 +422,11 @@ bool launch_line_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
     launch_pdl(ctx, kern, dim3(grid), dim3(kThreads), smem, k);
   };
   switch (mode) {
-    case StepMode::First: run(cheb_line_kernel<F, CH, R, MM, 0, RP, MINB, UNR>); break;
-    case StepMode::Step: run(cheb_line_kernel<F, CH, R, MM, 1, RP, MINB, UNR>); break;
-    case StepMode::Deg1: run(cheb_line_kernel<F, CH, R, MM, 2, RP, MINB, UNR>); break;
-    case StepMode::Spmm: run(cheb_line_kernel<F, CH, R, MM, 3, RP, MINB, UNR>); break;
-    case StepMode::SpmmAcc: run(cheb_line_kernel<F, CH, R, MM, 4, RP, MINB, UNR>); break;
+    case StepMode::First: run(cheb_line_kernel<F, CH, R, MM, 0, RP, MINB, UNR, MASK>); break;
+    case StepMode::Step: run(cheb_line_kernel<F, CH, R, MM, 1, RP, MINB, UNR, MASK>); break;
+    case StepMode::Deg1: run(cheb_line_kernel<F, CH, R, MM, 2, RP, MINB, UNR, MASK>); break;
+    case StepMode::Spmm: run(cheb_line_kernel<F, CH, R, MM, 3, RP, MINB, UNR, MASK>); break;
+    case StepMode::SpmmAcc: run(cheb_line_kernel<F, CH, R, MM, 4, RP, MINB, UNR, MASK>); break;
   }
   ADP_LAUNCH_CHECK();
   ctx->launches += 1;
@@ -762,18 +771,41 @@ bool dispatch_line(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
 }  // namespace
 
 // Automatic choice (variant 0): the line kernel where it measured faster than
-// the lean kernel (tools/tune_step.py, profiles/r01_kernel_evolution.md) --
-// long stencil rows (config 4: 27 entries, L1/L2-gather bound) or blocks that
-// stay L2-resident (config 1) -- when most row blocks share a shifted pattern.
-// DRAM-streaming short-row operators (config 2) stay on the lean kernel.
+// the lean kernel (tools/tune_step.py, profiles/r01_kernel_evolution.md): long
+// stencil rows (config 4: 27 entries, gather-latency bound) whose row blocks are
+// mostly shifted copies of one pattern. Short-row operators (configs 1-3, the
+// config-1 solve) stay on the lean kernel, which is faster there. A ragged
+// width runs as full 64-vector panels plus one masked launch for the rest.
 template <class F, class RP>
 bool auto_line(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
   const adp_csr* a = s.a;
-  const int64_t eb = a->dtype == ADP_C128 ? 16 : 8;
   const bool long_rows = a->nnz >= 12 * a->n_rows;
-  const bool l2_resident = a->n_rows * qv * 16 <= (int64_t{40} << 20);
-  if (!(long_rows || l2_resident) || qv % 64 != 0 || eb != 8 || ctx->panel_cols != 0) return false;
-  return launch_line_cfg<F, 2, 2, 3, RP, 3>(ctx, mode, s, qv, 0.5);
+  if (!long_rows || a->dtype != ADP_F64 || ctx->panel_cols != 0) return false;
+  const int64_t full = qv / 64 * 64, rem = qv - full;
+  if (full > 0) {
+    StepArgs t = s;
+    t.q = full * 2;
+    if (!launch_line_cfg<F, 2, 2, 3, RP, 3>(ctx, mode, t, full, 0.5)) return false;
+  } else if (get_line_plan(const_cast<adp_csr*>(a), 2, 3)->regular_frac < 0.5) {
+    return false;
+  }
+  if (rem > 0) {  // column-offset pointers, like the lean kernel's ragged split
+    StepArgs t = s;
+    const int64_t off = full * 16;
+    auto shift = [&](const void* ptr) -> void* {
+      return ptr ? const_cast<char*>(static_cast<const char*>(ptr) + off) : nullptr;
+    };
+    t.gsrc = shift(s.gsrc);
+    t.vin = shift(s.vin);
+    t.yin = shift(s.yin);
+    t.out = shift(s.out);
+    t.wout = shift(s.wout);
+    t.q = rem * 2;
+    const bool ok = rem <= 32 ? launch_line_cfg<F, 1, 2, 3, RP, 4, 1, true>(ctx, mode, t, rem, 0.0)
+                              : launch_line_cfg<F, 2, 2, 3, RP, 3, 1, true>(ctx, mode, t, rem, 0.0);
+    if (!ok) fail(ADP_ERR_RUNTIME, "line kernel: ragged tail launch failed");
+  }
+  return true;
 }
 
 bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
@@ -781,12 +813,11 @@ bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   if (s.row_begin != 0 || s.row_end != a->n_rows || a->n_rows >= (int64_t{1} << 30)) return false;
   const bool cplx = a->dtype == ADP_C128;
   const int epv = cplx ? 1 : 2;
-  if (s.q % epv != 0) return false;
-  const int64_t qv = s.q / epv;
+  const int64_t qv = (s.q + epv - 1) / epv;  // odd real widths: the padding column of the (even) ld rides along
   for (int64_t ld : {s.ld, s.ld_y, s.ld_out})
     if (ld % epv != 0 || (ld / epv) * 16 >= (int64_t{1} << 32)) return false;
   if (ctx->variant == 0) {
-    if (cplx) return false;
+    if (cplx || !ctx->auto_line) return false;
     return a->rp64 ? auto_line<RealN, int64_t>(ctx, mode, s, qv) : auto_line<RealN, int32_t>(ctx, mode, s, qv);
   }
   if (cplx) return a->rp64 ? dispatch_line<CplxN, int64_t>(ctx, mode, s, qv) : dispatch_line<CplxN, int32_t>(ctx, mode, s, qv);

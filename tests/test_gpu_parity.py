@@ -327,3 +327,22 @@ def test_kernel_variants_bitwise(ctx, orc, kind):
                     assert_bitwise(adp.maspmm(da, x), want_spmm)
         finally:
             ctx.set_tuning(0)
+
+
+def test_auto_line_kernel_ragged_widths(ctx, orc):
+    # the automatic line kernel (27-point stencil: long rows) on ragged and odd widths: full 64-vector
+    # panels + one masked launch, odd q through the padded leading dimension -- bitwise vs the oracle
+    from paper_2604_00914_b200 import configs
+
+    a = configs.dft_like_27pt(9, n_centres=4, seed=2)
+    n = a.n_rows
+    oa = orc.Csr(n, n, a.row_ptr, a.col_idx, a.values)
+    t = orc.Tiled(oa, 256, 64)
+    f, g = same_filter(orc, -0.3, 0.4, (-30.0, 30.0), 9)
+    da = adp.DeviceCsr(a, ctx)
+    rng = np.random.default_rng(5)
+    for q in (20, 33, 101, 150, 129):
+        x = np.asfortranarray(rng.standard_normal((n, q)))
+        for d in (1, 2, 9):
+            assert_bitwise(adp.clenshaw_apply(f, da, x, d), orc.clenshaw_apply(g, t, x, d))
+        assert_bitwise(adp.maspmm(da, x), orc.maspmm(t, x))

@@ -1,0 +1,70 @@
+"""Sample power / SM clock while a sustained clenshaw_apply_device loop runs (GPU).
+
+Usage: python tools/power_probe.py [--config c2] [--degree 3000] [--variant 0]
+Prints ms per degree step and the median power draw / SM clock during the run.
+"""
+import argparse
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_00914_b200 as adp  # noqa: E402
+from paper_2604_00914_b200 import configs  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", default="c2")
+    p.add_argument("--degree", type=int, default=3000)
+    p.add_argument("--variant", type=int, default=0)
+    args = p.parse_args()
+    cfg = configs.CONFIGS[args.config]
+    a = cfg.operator()
+    k1 = configs.filter_degree(cfg)
+    f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, max(args.degree, int(math.ceil(2.5 * k1))), 0.5)
+    ctx = adp.Context(0)
+    ctx.set_stream(torch.cuda.current_stream())
+    ctx.set_tuning(args.variant)
+    da = adp.DeviceCsr(a, ctx)
+    dt = torch.complex128 if a.is_complex else torch.float64
+    x = torch.randn(a.n_rows, cfg.q, dtype=dt, device="cuda")
+    y = torch.empty_like(x)
+    adp.clenshaw_apply_device(f, da, x, 50, out=y)
+    torch.cuda.synchronize()
+    samples, stop = [], threading.Event()
+
+    def sampler():
+        while not stop.is_set():
+            out = subprocess.run(["nvidia-smi", "--query-gpu=power.draw,clocks.sm,temperature.gpu",
+                                  "--format=csv,noheader,nounits", "-i", "0"], capture_output=True, text=True).stdout
+            try:
+                pw, sm, tc = (float(v) for v in out.strip().split(","))
+                samples.append((pw, sm, tc))
+            except ValueError:
+                pass
+            time.sleep(0.1)
+
+    th = threading.Thread(target=sampler)
+    th.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    adp.clenshaw_apply_device(f, da, x, args.degree, out=y)
+    e1.record()
+    torch.cuda.synchronize()
+    stop.set()
+    th.join()
+    ms = e0.elapsed_time(e1) / args.degree
+    s = sorted(samples[len(samples) // 4:])  # skip the ramp
+    med = lambda i: sorted(v[i] for v in s)[len(s) // 2] if s else float("nan")  # noqa: E731
+    print(f"{args.config} variant {args.variant}: {ms:.4f} ms/step, power {med(0):.0f} W, sm {med(1):.0f} MHz, "
+          f"temp {med(2):.0f} C ({len(samples)} samples)")
+
+
+if __name__ == "__main__":
+    main()
