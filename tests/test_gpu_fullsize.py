@@ -1,4 +1,4 @@
-"""Full-size parity on BASELINE.json's configurations 2, 3 and 4 (GPU).
+"""Full-size parity on BASELINE.json's configurations 2, 3 and 4 and config 5's structure (c5s) (GPU).
 
 The oracle cannot run a full n x q block at these sizes in seconds, but the
 step kernel computes every column independently: so the GPU result of the
@@ -46,7 +46,8 @@ def device_block(ctx, n, q, complex_=False, seed=3):
 
 @pytest.mark.parametrize("name,degree,cols", [("c2", 8, [(0, 2), (130, 132), (254, 256)]),
                                               ("c3", 6, [(0, 2), (383, 384)]),
-                                              ("c4", 4, [(0, 2), (1022, 1024)])])
+                                              ("c4", 4, [(0, 2), (1022, 1024)]),
+                                              ("c5s", 3, [(0, 1), (200, 201), (383, 384)])])
 def test_full_size_columns_bitwise_vs_oracle(ctx, orc, name, degree, cols):
     cfg = configs.CONFIGS[name]
     a = cfg.operator()
