@@ -98,6 +98,14 @@ adp_status adp_ctx_set_tile_config(adp_ctx* ctx, int32_t chunks, int32_t stages,
  * order (tiled_matrix.hpp:78-81,200). */
 adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
                           const int64_t* col_idx, const void* values, adp_dtype dtype, adp_csr** out);
+/* As adp_csr_create, from arrays already in device memory of ctx's device (a GPU-side
+ * generator or loader: config 5's 2.16 G-nonzero operator never exists on the host).
+ * d_row_ptr: int64[n_rows+1], d_col_idx: int32[nnz], d_values: double[nnz] or complex128[nnz].
+ * Validated on the device like CsrMatrix::validate (csr_matrix.hpp:101-116): row_ptr
+ * non-decreasing from 0 to nnz, columns strictly increasing within a row and in range.
+ * The arrays are copied (the caller keeps and may free them after the call returns). */
+adp_status adp_csr_create_device(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* d_row_ptr,
+                                 const int32_t* d_col_idx, const void* d_values, adp_dtype dtype, adp_csr** out);
 adp_status adp_csr_destroy(adp_csr* a);
 adp_status adp_csr_info(const adp_csr* a, int64_t* n_rows, int64_t* n_cols, int64_t* nnz, int32_t* dtype);
 

@@ -83,6 +83,7 @@ SIGNATURES = {
     "adp_ctx_set_tuning": (I32, [P, I32]),
     "adp_ctx_set_tile_config": (I32, [P, I32, I32, I32, I32]),
     "adp_csr_create": (I32, [P, I64, I64, P, P, P, I32, P]),
+    "adp_csr_create_device": (I32, [P, I64, I64, I64, P, P, P, I32, P]),
     "adp_csr_destroy": (I32, [P]),
     "adp_csr_info": (I32, [P, P, P, P, P]),
     "adp_filter_apply": (I32, [P, P, P, I32, D, D, I32, P, I64, I64, I64, I32, P, I64, P]),

@@ -152,6 +152,7 @@ struct adp_csr {
   std::vector<int64_t> h_row_ptr;
   std::vector<int32_t> h_col;
   void* h_values = nullptr;  // malloc'd copy of the values
+  bool host_ready = false;   // h_* filled (eagerly by adp_csr_create, lazily for device-created operators)
   std::vector<std::unique_ptr<adp::Tiling>> tilings;
   std::vector<std::unique_ptr<adp::Segments>> segments;
   std::vector<std::unique_ptr<adp::PairPlan>> pair_plans;
@@ -240,6 +241,14 @@ PairPlan* get_pair_plan(adp_csr* a, int64_t chunk_rows, int64_t gs, int64_t n_pa
 // blocks of rows with shifted column patterns. Returns false if not applicable.
 bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 const LinePlan* get_line_plan(adp_csr* a, int rows_per_block, int max_run);
+// Host copies of a device-created operator's arrays, downloaded on first use by the
+// host-side preprocessing (line plans, tilings, segments, the dense fallback).
+void ensure_host_copy(adp_csr* a);
+// Device-side CSR validation (CsrMatrix::validate, csr_matrix.hpp:101-116): returns 0 if
+// row_ptr is non-decreasing from 0 to nnz and every row's columns are strictly increasing in [0, n_cols).
+int validate_csr_device(adp_ctx* ctx, const int64_t* row_ptr, const int32_t* col, int64_t n_rows, int64_t n_cols,
+                        int64_t nnz);
+void narrow_row_ptr_device(adp_ctx* ctx, const int64_t* src, int32_t* dst, int64_t count);
 
 // Column segments of R-row blocks (segments.cpp); built once per (operator, R).
 const Segments* get_segments(adp_csr* a, int rows_per_block);

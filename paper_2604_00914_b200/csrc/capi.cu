@@ -283,7 +283,7 @@ adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
     if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) ||
         (variant > 24 && variant < 31) || (variant > 33 && variant < 41) || (variant > 46 && variant < 51) ||
         (variant > 56 && variant < 61) || (variant > 66 && variant < 71) || (variant > 76 && variant < 81) ||
-        variant > 98)
+        (variant > 98 && variant < 101) || variant > 108)
       fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
     ctx->pair_variant = (variant > 70 && variant < 77) ? variant - 70 : 0;
@@ -358,6 +358,7 @@ adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const in
       a->h_values = std::malloc(std::max<size_t>(nnz, 1) * eb);
       if (!a->h_values) throw std::bad_alloc();
       if (nnz) std::memcpy(a->h_values, values, nnz * eb);
+      a->host_ready = true;
     } catch (...) {
       std::free(a->h_values);
       cudaFree(a->row_ptr);
@@ -369,6 +370,54 @@ adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const in
     *out = a;
   });
 }
+
+adp_status adp_csr_create_device(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* d_row_ptr,
+                                 const int32_t* d_col_idx, const void* d_values, adp_dtype dtype, adp_csr** out) {
+  return guarded([&] {
+    if (n_rows < 0 || n_cols < 0 || nnz < 0) fail(ADP_ERR_DIMENSION, "negative matrix size");
+    if (n_cols > std::numeric_limits<int32_t>::max() || n_rows > std::numeric_limits<int32_t>::max())
+      fail(ADP_ERR_DIMENSION, "adp_csr_create_device: dimension exceeds int32 column indexing");
+    if (dtype != ADP_F64 && dtype != ADP_C128) fail(ADP_ERR_CONFIG, "adp_csr_create_device: unknown dtype");
+    set_device(ctx);
+    const int bad = adp::validate_csr_device(ctx, d_row_ptr, d_col_idx, n_rows, n_cols, nnz);
+    if (bad & 1) fail(ADP_ERR_DIMENSION, "row_ptr not non-decreasing from 0 to nnz");
+    if (bad & 2) fail(ADP_ERR_DIMENSION, "column index out of range");
+    if (bad & 4) fail(ADP_ERR_DIMENSION, "columns not strictly increasing within a row");
+    auto* a = new adp_csr;
+    a->ctx = ctx;
+    a->device = ctx->device;
+    a->n_rows = n_rows;
+    a->n_cols = n_cols;
+    a->nnz = nnz;
+    a->dtype = dtype;
+    const char* force64 = std::getenv("ADP_FORCE_RP64");
+    a->rp64 = nnz > std::numeric_limits<int32_t>::max() || (force64 && force64[0] == '1');
+    const size_t eb = dtype == ADP_C128 ? 16 : 8;
+    try {
+      const size_t rp_bytes = (n_rows + 1) * (a->rp64 ? 8 : 4);
+      ADP_CUDA(cudaMalloc(&a->row_ptr, rp_bytes));
+      ADP_CUDA(cudaMalloc(reinterpret_cast<void**>(&a->col_idx), std::max<size_t>(nnz, 1) * 4));
+      ADP_CUDA(cudaMalloc(&a->values, std::max<size_t>(nnz, 1) * eb));
+      if (a->rp64)
+        ADP_CUDA(cudaMemcpyAsync(a->row_ptr, d_row_ptr, rp_bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+      else
+        adp::narrow_row_ptr_device(ctx, d_row_ptr, static_cast<int32_t*>(a->row_ptr), n_rows + 1);
+      if (nnz) {
+        ADP_CUDA(cudaMemcpyAsync(a->col_idx, d_col_idx, nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        ADP_CUDA(cudaMemcpyAsync(a->values, d_values, nnz * eb, cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+      ADP_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      cudaFree(a->row_ptr);
+      cudaFree(a->col_idx);
+      cudaFree(a->values);
+      delete a;
+      throw;
+    }
+    *out = a;
+  });
+}
+
 
 adp_status adp_csr_destroy(adp_csr* a) {
   return guarded([&] {

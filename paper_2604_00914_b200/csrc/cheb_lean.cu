@@ -278,6 +278,167 @@ void launch_lean(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
   ctx->launches += 1;
 }
 
+// ---- multi-row lean kernel ---------------------------------------------------------------
+// cheb_lean_kernel's arithmetic and data movement, but each group walks RPW rows
+// of its panel instead of one: the prologue (task decomposition, mbarrier init,
+// cache policy) is paid once per RPW rows, the next row's row_ptr entry is the
+// current row's end, and the next row's V / Y panels are bulk-copied into the
+// group's (single) slot as soon as the epilogue has read it, so they land while
+// the next row's gathers are in flight. STRD: the CTA's groups take rows
+// rb + i*kGroups + grp (the 8 warps of a CTA work on 8 consecutive rows at any
+// time, as in the one-row kernel, sharing x-neighbour gathers through L1);
+// otherwise rows rb + grp*RPW + i (each warp re-gathers its previous row's
+// neighbours). Rows are independent, so every bit of the result is unchanged.
+template <class F, int G, int CH, int RPW, bool STRD, int MODE, class RP, int MINB, bool MASK = false>
+__global__ void __launch_bounds__(kThreads, MINB) cheb_leanm_kernel(const LArgs p) {
+  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
+  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
+  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
+  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
+  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
+  constexpr int kGroups = kThreads / G;
+  constexpr int kRowsPerCta = kGroups * RPW;
+  constexpr uint32_t kPB = G * CH * 16u;
+  extern __shared__ __align__(16) uint8_t smem[];
+
+  const int grp = threadIdx.x / G, lane = threadIdx.x % G;
+  const uint32_t gmask = G == 32 ? 0xffffffffu : (((1u << (G % 32)) - 1u) << ((threadIdx.x % 32) / G * G));
+  const int32_t nrows = static_cast<int32_t>(p.nrows);
+  const int32_t nblk = (nrows + kRowsPerCta - 1) / kRowsPerCta;
+  const int32_t panel = static_cast<int32_t>(blockIdx.x) / nblk;  // CTA-uniform
+  const int32_t rb = (static_cast<int32_t>(blockIdx.x) - panel * nblk) * kRowsPerCta;
+  auto rel_row = [&](int i) -> int32_t { return STRD ? rb + i * kGroups + grp : rb + grp * RPW + i; };
+  int32_t rel = rel_row(0);
+  if (rel >= nrows) return;  // group-uniform
+  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
+  const uint32_t voff = poff + lane * 16u;
+  const uint64_t pol = policy_evict_first(1.0f);
+
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + grp;
+  double2* my = reinterpret_cast<double2*>(smem + ((kGroups * 8 + 15) / 16) * 16) + grp * (2 * G * CH);
+  int64_t r = p.row_begin + rel;
+  RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r));
+  RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r + 1));
+  pdl_wait_and_release();
+  bool ok[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) ok[c] = !MASK || c * G + lane < p.valid;
+  const uint32_t cpb = MASK ? static_cast<uint32_t>(p.valid) * 16u : kPB;
+  if constexpr (kStep) {
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      mbar_arrive_expect_tx(bar, 2 * cpb);
+      bulk_g2s_hint(my, p.vin + static_cast<uint64_t>(r) * p.ldg_b + poff, cpb, bar, pol);
+      bulk_g2s_hint(my + G * CH, p.yin + static_cast<uint64_t>(r) * p.ldy_b + poff, cpb, bar, pol);
+    }
+  }
+  const char* gb = p.g + voff;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (int i = 0; i < RPW; ++i) {
+    char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
+    double2 acc[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if constexpr (kSpmmAcc)
+        acc[c] = ok[c] ? *reinterpret_cast<const double2*>(ob + G * 16 * c) : make_double2(0.0, 0.0);
+      else
+        acc[c] = make_double2(0.0, 0.0);
+    }
+    for (RP e = start; e < end; ++e) {
+      const int cidx = __ldg(p.col + e);
+      const auto v = F::load(p.val, static_cast<int64_t>(e));
+      const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
+      double2 w[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) w[c] = ok[c] ? __ldg(src + G * c) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        double2 wv = w[c];
+        if constexpr (kFirst) wv = scale2(p.s2, wv);
+        acc[c] = F::mac(acc[c], v, wv);
+      }
+    }
+    // next row of this group (its row_ptr end is loaded before the epilogue's stores)
+    const int32_t nrel = i + 1 < RPW ? rel_row(i + 1) : nrows;
+    const bool more = nrel < nrows;
+    if (more) {
+      start = end;
+      if (STRD) start = static_cast<RP>(ld_rp<RP>(p.row_ptr, p.row_begin + nrel));
+      end = static_cast<RP>(ld_rp<RP>(p.row_ptr, p.row_begin + nrel + 1));
+    }
+    if constexpr (kStep) {
+      __syncwarp(gmask);
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    }
+    const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
+    char* wb = kFirst ? p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff : nullptr;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (!ok[c]) continue;
+      double2 own = make_double2(0.0, 0.0);
+      if constexpr (kNeedOwn) own = __ldg(own_src + G * c);
+      double2 res;
+      if constexpr (kStep) {
+        const double2 vv = my[c * G + lane];
+        const double2 yy = my[G * CH + c * G + lane];
+        res = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
+      } else if constexpr (kFirst) {
+        const double2 wn = scale2(p.s2, own);
+        st_hint(wb + G * 16 * c, wn, pol);
+        res = add2(scale2(p.s0, acc[c]), scale2(p.s1, wn));
+      } else if constexpr (kDeg1) {
+        res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own))));
+      } else {
+        res = acc[c];
+      }
+      st_hint(ob + G * 16 * c, res, pol);
+    }
+    if (!more) break;  // group-uniform
+    r = p.row_begin + nrel;
+    if constexpr (kStep) {
+      // the slot is free once every lane of the group has read it: refill it with the next row
+      __syncwarp(gmask);
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive_expect_tx(bar, 2 * cpb);
+        bulk_g2s_hint(my, p.vin + static_cast<uint64_t>(r) * p.ldg_b + poff, cpb, bar, pol);
+        bulk_g2s_hint(my + G * CH, p.yin + static_cast<uint64_t>(r) * p.ldy_b + poff, cpb, bar, pol);
+      }
+    }
+  }
+}
+
+template <class F, int G, int CH, int RPW, bool STRD, class RP, int MINB, bool MASK = false>
+void launch_leanm(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
+  constexpr int kGroups = kThreads / G;
+  k.n_panels = MASK ? 1 : qv / (G * CH);
+  k.valid = static_cast<int32_t>(qv);
+  const int64_t nblk = (k.nrows + kGroups * RPW - 1) / (kGroups * RPW);
+  const int64_t grid64 = nblk * k.n_panels;
+  if (grid64 >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_leanm: too many CTAs");
+  const int grid = static_cast<int>(grid64);
+  const size_t smem = mode == StepMode::Step
+                          ? static_cast<size_t>((kGroups * 8 + 15) / 16) * 16 + static_cast<size_t>(kGroups) * 2 * G * CH * 16
+                          : 16;
+  auto run = [&](auto kern) {
+    if (smem > 48 * 1024)
+      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    launch_pdl(ctx, kern, dim3(grid), dim3(kThreads), smem, k);
+  };
+  switch (mode) {
+    case StepMode::First: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 0, RP, MINB, MASK>); break;
+    case StepMode::Step: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 1, RP, MINB, MASK>); break;
+    case StepMode::Deg1: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 2, RP, MINB, MASK>); break;
+    case StepMode::Spmm: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 3, RP, MINB, MASK>); break;
+    case StepMode::SpmmAcc: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 4, RP, MINB, MASK>); break;
+  }
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
+}
+
 // ---- row-block union kernel -----------------------------------------------------------
 // A warp owns R consecutive rows of one panel and walks the UNION of their
 // column sets in ascending order: every distinct W row panel is gathered once
@@ -946,6 +1107,15 @@ void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_
     case 64: if (qv % 128 == 0) return launch_win<F, 4, 32, 1, RP, 1>(ctx, mode, k, qv); break;
     case 65: if (qv % 64 == 0) return launch_win<F, 2, 16, 1, RP, 3>(ctx, mode, k, qv); break;
     case 66: if (qv % 128 == 0) return launch_win<F, 4, 4, 1, RP, 8>(ctx, mode, k, qv); break;
+    // multi-row lean kernel (tuning variants 101-108)
+    case 101: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 2, true, RP, 4>(ctx, mode, k, qv); break;
+    case 102: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 4, true, RP, 4>(ctx, mode, k, qv); break;
+    case 103: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 8, true, RP, 4>(ctx, mode, k, qv); break;
+    case 104: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 2, false, RP, 4>(ctx, mode, k, qv); break;
+    case 105: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 4, false, RP, 4>(ctx, mode, k, qv); break;
+    case 106: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 8, false, RP, 4>(ctx, mode, k, qv); break;
+    case 107: if (qv % 64 == 0) return launch_leanm<F, 32, 2, 4, true, RP, 6>(ctx, mode, k, qv); break;
+    case 108: if (qv % 64 == 0) return launch_leanm<F, 32, 2, 4, false, RP, 6>(ctx, mode, k, qv); break;
     default: break;
   }
   if (qv % 128 == 0 && cap >= 128) return launch_lean<F, 32, 4, 1, RP, 4>(ctx, mode, k, qv);

@@ -46,6 +46,7 @@ const LinePlan* get_line_plan(adp_csr* a, int R, int mm) {
   p->mm = mm;
   const int64_t n = a->n_rows;
   const int64_t nb = (n + R - 1) / R;
+  ensure_host_copy(a);
   const std::vector<int64_t>& rp = a->h_row_ptr;
   const std::vector<int32_t>& ci = a->h_col;
   std::vector<int32_t> blk_pat(static_cast<size_t>(nb), -1);

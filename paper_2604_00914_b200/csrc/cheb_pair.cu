@@ -360,6 +360,7 @@ PairPlan* get_pair_plan(adp_csr* a, int64_t chunk_rows, int64_t gs, int64_t n_pa
     const int64_t nch = (n + chunk_rows - 1) / chunk_rows;
     std::vector<int64_t> lo(nch), hi(nch);
     for (int64_t k = 0; k < nch; ++k) lo[k] = hi[k] = k;
+    ensure_host_copy(const_cast<adp_csr*>(a));
     const std::vector<int64_t>& rp = a->h_row_ptr;
     const std::vector<int32_t>& ci = a->h_col;
     for (int64_t r = 0; r < n; ++r) {

@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <new>
+#include <vector>
 
 #include "adp_internal.hpp"
 
@@ -172,6 +175,88 @@ void launch_fill_philox(adp_ctx* ctx, double* dst, int64_t n, int64_t q, int64_t
   fill_philox_kernel<<<grid_for(ctx, n * q, 256), 256, 0, ctx->stream>>>(dst, n, q, ld, seed, stream, kind);
   ADP_LAUNCH_CHECK();
   ctx->launches += 1;
+}
+
+// ---- device-side CSR checks (adp_csr_create_device) ---------------------------------------
+namespace {
+
+// One thread per row: bit 0 = row_ptr decreasing or endpoints wrong, bit 1 = column out of
+// range, bit 2 = columns not strictly increasing (the CsrMatrix invariant, csr_matrix.hpp:101-116).
+__global__ void validate_csr_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t n_rows,
+                                    int64_t n_cols, int64_t nnz, int* __restrict__ flags) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int bad = 0;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n_rows; r += stride) {
+    const int64_t b = rp[r], e = rp[r + 1];
+    if (e < b || b < 0 || e > nnz || (r == 0 && b != 0) || (r == n_rows - 1 && e != nnz)) {
+      bad |= 1;
+      continue;
+    }
+    int32_t prev = -1;
+    for (int64_t k = b; k < e; ++k) {
+      const int32_t c = col[k];
+      if (c < 0 || c >= n_cols) bad |= 2;
+      if (k > b && c <= prev) bad |= 4;
+      prev = c;
+    }
+  }
+  if (bad) atomicOr(flags, bad);
+}
+
+__global__ void narrow_kernel(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t count) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)
+    dst[i] = static_cast<int32_t>(src[i]);
+}
+
+}  // namespace
+
+int validate_csr_device(adp_ctx* ctx, const int64_t* row_ptr, const int32_t* col, int64_t n_rows, int64_t n_cols,
+                        int64_t nnz) {
+  int* flags = nullptr;
+  ADP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int), ctx->stream));
+  ADP_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), ctx->stream));
+  int h = 0;
+  if (n_rows > 0) {
+    validate_csr_kernel<<<grid_for(ctx, n_rows, 256), 256, 0, ctx->stream>>>(row_ptr, col, n_rows, n_cols, nnz, flags);
+    ADP_LAUNCH_CHECK();
+    ctx->launches += 1;
+  }
+  ADP_CUDA(cudaMemcpyAsync(&h, flags, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  ADP_CUDA(cudaFreeAsync(flags, ctx->stream));
+  ADP_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h;
+}
+
+void narrow_row_ptr_device(adp_ctx* ctx, const int64_t* src, int32_t* dst, int64_t count) {
+  if (count == 0) return;
+  narrow_kernel<<<grid_for(ctx, count, 256), 256, 0, ctx->stream>>>(src, dst, count);
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
+}
+
+void ensure_host_copy(adp_csr* a) {
+  if (a->host_ready) return;
+  const size_t eb = a->dtype == ADP_C128 ? 16 : 8;
+  ADP_CUDA(cudaSetDevice(a->device));
+  ADP_CUDA(cudaDeviceSynchronize());
+  a->h_row_ptr.resize(a->n_rows + 1);
+  if (a->rp64) {
+    ADP_CUDA(cudaMemcpy(a->h_row_ptr.data(), a->row_ptr, (a->n_rows + 1) * 8, cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<int32_t> rp32(a->n_rows + 1);
+    ADP_CUDA(cudaMemcpy(rp32.data(), a->row_ptr, (a->n_rows + 1) * 4, cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r <= a->n_rows; ++r) a->h_row_ptr[r] = rp32[r];
+  }
+  a->h_col.resize(a->nnz);
+  void* hv = std::malloc(std::max<size_t>(a->nnz, 1) * eb);
+  if (!hv) throw std::bad_alloc();
+  if (a->nnz) {
+    ADP_CUDA(cudaMemcpy(a->h_col.data(), a->col_idx, a->nnz * 4, cudaMemcpyDeviceToHost));
+    ADP_CUDA(cudaMemcpy(hv, a->values, a->nnz * eb, cudaMemcpyDeviceToHost));
+  }
+  a->h_values = hv;
+  a->host_ready = true;
 }
 
 }  // namespace adp

@@ -35,6 +35,7 @@ const Segments* get_segments(adp_csr* a, int R) {
   const int64_t n = a->n_rows;
   const int64_t vb = a->dtype == ADP_C128 ? 16 : 8;
   const int64_t nb = (n + R - 1) / R;
+  ensure_host_copy(a);
   const std::vector<int64_t>& rp = a->h_row_ptr;
   const std::vector<int32_t>& ci = a->h_col;
   const auto* hv = static_cast<const uint8_t*>(a->h_values);

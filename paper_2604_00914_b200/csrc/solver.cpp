@@ -329,6 +329,7 @@ adp_solve_result* solve(adp_ctx* ctx, const adp_csr* a, const adp_solver_config&
 
   if (p >= n) {  // dense fallback (solver.cpp:178-198)
     std::vector<double> dense(static_cast<size_t>(n) * n, 0.0);
+    ensure_host_copy(const_cast<adp_csr*>(a));
     const double* hv = static_cast<const double*>(a->h_values);
     for (int64_t r = 0; r < n; ++r)
       for (int64_t k = a->h_row_ptr[r]; k < a->h_row_ptr[r + 1]; ++k) dense[r + static_cast<size_t>(a->h_col[k]) * n] += hv[k];

@@ -43,6 +43,7 @@ const Tiling* get_tiling(adp_csr* a, int64_t panel_bytes, int64_t stage_bytes) {
   t->stage_bytes = stage_bytes;
   const int64_t n = a->n_rows;
   const int64_t vb = a->dtype == ADP_C128 ? 16 : 8;
+  ensure_host_copy(a);
   const std::vector<int64_t>& rp = a->h_row_ptr;
   const std::vector<int32_t>& ci = a->h_col;
   std::vector<int32_t> tile_row{0};

@@ -12,7 +12,7 @@ import ctypes as C
 
 import numpy as np
 
-from ._native import ADP_C128, ADP_COL_MAJOR, ADP_F64, ADP_ROW_MAJOR, DimensionError, check, lib
+from ._native import ADP_C128, ADP_COL_MAJOR, ADP_F64, ADP_ROW_MAJOR, ConfigError, DimensionError, check, lib
 from .filter import ChebFilter
 from .sparse import CsrMatrix
 
@@ -101,6 +101,32 @@ class DeviceCsr:
                                    C.byref(h)))
         self.h = h
         self.nnz = int(rp[-1])
+
+    @classmethod
+    def from_device(cls, n_rows: int, n_cols: int, row_ptr, col_idx, values, ctx: Context | None = None) -> "DeviceCsr":
+        """adp_csr_create_device: an operator from CUDA tensors (int64 row_ptr, int32 col_idx, float64 or
+        complex128 values) already on ctx's device -- for operators generated on the GPU (config 5).
+        Validated on the device like CsrMatrix::validate; the tensors are copied."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        if str(values.dtype) not in ("torch.float64", "torch.complex128"):
+            raise ConfigError("DeviceCsr.from_device: values must be float64 or complex128")
+        if str(row_ptr.dtype) != "torch.int64" or str(col_idx.dtype) != "torch.int32":
+            raise ConfigError("DeviceCsr.from_device: row_ptr must be int64 and col_idx int32")
+        for t in (row_ptr, col_idx, values):
+            if not t.is_cuda or not t.is_contiguous():
+                raise ConfigError("DeviceCsr.from_device: arrays must be contiguous CUDA tensors")
+        if row_ptr.numel() != self.n_rows + 1 or col_idx.numel() != values.numel():
+            raise DimensionError("DeviceCsr.from_device: array sizes do not match the dimensions")
+        self.is_complex = str(values.dtype) == "torch.complex128"
+        self.nnz = int(col_idx.numel())
+        h = C.c_void_p()
+        check(lib().adp_csr_create_device(self.ctx.h, self.n_rows, self.n_cols, self.nnz, C.c_void_p(row_ptr.data_ptr()),
+                                          C.c_void_p(col_idx.data_ptr()), C.c_void_p(values.data_ptr()),
+                                          ADP_C128 if self.is_complex else ADP_F64, C.byref(h)))
+        self.h = h
+        return self
 
     @property
     def dtype(self):

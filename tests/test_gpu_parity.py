@@ -286,7 +286,8 @@ def test_config2_full_size_bitwise_low_degree(ctx, orc):
 # equal to the oracle: they only reorganise loads, never the per-element
 # arithmetic. Stencil operators exercise the shifted-pattern blocks (and their
 # irregular faces), a random matrix the row-by-row fallbacks.
-VARIANTS = [0, 1, 11, 21, 22, 31, 33, 41, 42, 51, 56, 61, 62, 64, 71, 72, 73, 81, 82, 83, 84, 86, 88, 91, 92, 94, 97]
+VARIANTS = [0, 1, 11, 21, 22, 31, 33, 41, 42, 51, 56, 61, 62, 64, 71, 72, 73, 81, 82, 83, 84, 86, 88, 91, 92, 94, 97,
+            101, 102, 103, 104, 105, 106, 107, 108]
 
 
 @pytest.mark.parametrize("kind", ["lap7", "lap27", "random", "hermitian"])
@@ -346,3 +347,59 @@ def test_auto_line_kernel_ragged_widths(ctx, orc):
         for d in (1, 2, 9):
             assert_bitwise(adp.clenshaw_apply(f, da, x, d), orc.clenshaw_apply(g, t, x, d))
         assert_bitwise(adp.maspmm(da, x), orc.maspmm(t, x))
+
+
+# --------------------------------------------- operators created from device arrays ---
+def _torch_csr(a):
+    return (torch.from_numpy(np.asarray(a.row_ptr, np.int64)).cuda(),
+            torch.from_numpy(np.asarray(a.col_idx, np.int32)).cuda(),
+            torch.from_numpy(np.asarray(a.values)).cuda())
+
+
+def test_device_created_operator_bitwise(ctx, orc, monkeypatch):
+    # adp_csr_create_device: same results as the host-created operator, int32 and forced int64 offsets,
+    # real and complex, including the line kernel (27-point stencil: its plan needs the lazy host copy)
+    from paper_2604_00914_b200 import configs
+
+    lap27 = configs.dft_like_27pt(9, n_centres=4, seed=1)
+    herm = random_hermitian(150, 0.05, 4)
+    for force in ("0", "1"):
+        monkeypatch.setenv("ADP_FORCE_RP64", force)
+        for a in (lap27, herm):
+            n = a.n_rows
+            oa = orc.Csr(n, n, a.row_ptr, a.col_idx, a.values)
+            f, g = same_filter(orc, -0.3, 0.4, (-30.0, 30.0), 12)
+            da = adp.DeviceCsr.from_device(n, n, *_torch_csr(a), ctx=ctx)
+            assert da.nnz == a.nnz and da.is_complex == a.is_complex
+            rng = np.random.default_rng(n)
+            for q in (17, 128):
+                x = rng.standard_normal((n, q))
+                if a.is_complex:
+                    x = x + 1j * rng.standard_normal((n, q))
+                x = np.asfortranarray(x)
+                for d in (1, 2, 12):
+                    assert_bitwise(adp.clenshaw_apply(f, da, x, d), orc.clenshaw_apply(g, orc.Tiled(oa, 256, 64), x, d))
+            da.close()
+
+
+def test_device_created_operator_validation(ctx):
+    # CsrMatrix::validate (csr_matrix.hpp:101-116) on the device: DimensionError for each broken invariant
+    a = adp.CsrMatrix.from_triplets(4, 4, [0, 0, 1, 2, 3], [0, 2, 1, 2, 3], [1.0, 2.0, 3.0, 4.0, 5.0])
+    rp, ci, v = _torch_csr(a)
+    ok = adp.DeviceCsr.from_device(4, 4, rp, ci, v, ctx=ctx)
+    ok.close()
+    bad_cols = [ci.clone(), ci.clone(), ci.clone()]
+    bad_cols[0][1] = 0  # not strictly increasing
+    bad_cols[1][4] = 4  # out of range
+    bad_cols[2][0] = -1
+    for c in bad_cols:
+        with pytest.raises(adp.DimensionError):
+            adp.DeviceCsr.from_device(4, 4, rp, c, v, ctx=ctx)
+    bad_rp = rp.clone()
+    bad_rp[2] = 1  # decreasing
+    with pytest.raises(adp.DimensionError):
+        adp.DeviceCsr.from_device(4, 4, bad_rp, ci, v, ctx=ctx)
+    with pytest.raises(adp.ConfigError):
+        adp.DeviceCsr.from_device(4, 4, rp, ci.to(torch.int64), v, ctx=ctx)
+    with pytest.raises(adp.DimensionError):
+        adp.DeviceCsr.from_device(5, 5, rp, ci, v, ctx=ctx)

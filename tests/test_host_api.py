@@ -165,3 +165,27 @@ def test_mm_reference_fixtures_match_golden(golden_dir):
         z = np.load(f"{golden_dir}/fixture_{name}.npz")
         assert np.array_equal(a.row_ptr, z["row_ptr"]) and np.array_equal(a.col_idx, z["col_idx"])
         assert np.array_equal(a.values, z["values"])
+
+
+def test_config5_device_generator_structure():
+    # random_banded_hermitian_device (config 5's GPU generator) run on the CPU at a small size:
+    # exactly Hermitian, columns strictly ascending per row, the full band present, real diagonal
+    torch = pytest.importorskip("torch")
+    from paper_2604_00914_b200 import configs
+
+    n, hb, off = 2500, 17, 5
+    rp, ci, v = configs.random_banded_hermitian_device(n, hb, off, seed=2, chunk_rows=600, device="cpu")
+    assert rp.dtype == torch.int64 and ci.dtype == torch.int32 and v.dtype == torch.complex128
+    rp, ci, v = rp.numpy(), ci.numpy().astype(np.int64), v.numpy()
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    same_row = np.diff(rows) == 0
+    assert (np.diff(ci)[same_row] > 0).all()
+    d = np.zeros((n, n), complex)
+    d[rows, ci] = v
+    assert np.array_equal(d, d.conj().T)
+    band = np.abs(rows - ci) <= hb
+    assert band.sum() == sum(min(r, hb) + 1 + min(n - 1 - r, hb) for r in range(n))
+    assert (np.diag(d).imag == 0).all() and (np.diag(d) != 0).all()
+    assert 0.8 * 2 * off * n < (~band).sum() <= 2 * off * n
+    a = adp.CsrMatrix(n, n, rp, ci, v)  # the host CsrMatrix invariant holds too
+    assert a.nnz == len(v)

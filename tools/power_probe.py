@@ -18,12 +18,59 @@ import paper_2604_00914_b200 as adp  # noqa: E402
 from paper_2604_00914_b200 import configs  # noqa: E402
 
 
+def sampler(samples, stop):
+    while not stop.is_set():
+        out = subprocess.run(["nvidia-smi", "--query-gpu=power.draw,clocks.sm,temperature.gpu",
+                              "--format=csv,noheader,nounits", "-i", "0"], capture_output=True, text=True).stdout
+        try:
+            pw, sm, tc = (float(v) for v in out.strip().split(","))
+            samples.append((pw, sm, tc))
+        except ValueError:
+            pass
+        time.sleep(0.1)
+
+
+def summarize(samples):
+    s = samples[len(samples) // 4:]  # skip the ramp
+    med = lambda i: sorted(v[i] for v in s)[len(s) // 2] if s else float("nan")  # noqa: E731
+    return f"power {med(0):.0f} W, sm {med(1):.0f} MHz, temp {med(2):.0f} C ({len(samples)} samples)"
+
+
+def copy_probe(seconds):
+    a = torch.empty(1 << 28, dtype=torch.float64, device="cuda").normal_()
+    b = torch.empty_like(a)
+    b.copy_(a)
+    torch.cuda.synchronize()
+    samples, stop = [], threading.Event()
+    th = threading.Thread(target=sampler, args=(samples, stop))
+    th.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0, n = time.time(), 0
+    e0.record()
+    while time.time() - t0 < seconds:
+        for _ in range(50):
+            b.copy_(a)
+        n += 50
+        torch.cuda.synchronize()
+    e1.record()
+    torch.cuda.synchronize()
+    stop.set()
+    th.join()
+    gbs = 2 * a.numel() * 8 * n / (e0.elapsed_time(e1) * 1e6)
+    print(f"copy 2 GiB: {gbs:.0f} GB/s sustained, {summarize(samples)}")
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="c2")
     p.add_argument("--degree", type=int, default=3000)
     p.add_argument("--variant", type=int, default=0)
+    p.add_argument("--panel", type=int, default=0, help="lean panel cap in columns (0 = automatic)")
+    p.add_argument("--copy", type=float, default=0.0,
+                   help="instead: sustained torch copy of two 2 GiB buffers for this many seconds (HBM-only reference)")
     args = p.parse_args()
+    if args.copy > 0:
+        return copy_probe(args.copy)
     cfg = configs.CONFIGS[args.config]
     a = cfg.operator()
     k1 = configs.filter_degree(cfg)
@@ -31,6 +78,7 @@ def main():
     ctx = adp.Context(0)
     ctx.set_stream(torch.cuda.current_stream())
     ctx.set_tuning(args.variant)
+    ctx.set_panel(args.panel)
     da = adp.DeviceCsr(a, ctx)
     dt = torch.complex128 if a.is_complex else torch.float64
     x = torch.randn(a.n_rows, cfg.q, dtype=dt, device="cuda")
@@ -38,19 +86,7 @@ def main():
     adp.clenshaw_apply_device(f, da, x, 50, out=y)
     torch.cuda.synchronize()
     samples, stop = [], threading.Event()
-
-    def sampler():
-        while not stop.is_set():
-            out = subprocess.run(["nvidia-smi", "--query-gpu=power.draw,clocks.sm,temperature.gpu",
-                                  "--format=csv,noheader,nounits", "-i", "0"], capture_output=True, text=True).stdout
-            try:
-                pw, sm, tc = (float(v) for v in out.strip().split(","))
-                samples.append((pw, sm, tc))
-            except ValueError:
-                pass
-            time.sleep(0.1)
-
-    th = threading.Thread(target=sampler)
+    th = threading.Thread(target=sampler, args=(samples, stop))
     th.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -60,10 +96,8 @@ def main():
     stop.set()
     th.join()
     ms = e0.elapsed_time(e1) / args.degree
-    s = sorted(samples[len(samples) // 4:])  # skip the ramp
-    med = lambda i: sorted(v[i] for v in s)[len(s) // 2] if s else float("nan")  # noqa: E731
-    print(f"{args.config} variant {args.variant}: {ms:.4f} ms/step, power {med(0):.0f} W, sm {med(1):.0f} MHz, "
-          f"temp {med(2):.0f} C ({len(samples)} samples)")
+    b_step = a.nnz * ((16 if a.is_complex else 8) + 4) + (a.n_rows + 1) * 4 + 4 * a.n_rows * cfg.q * (16 if a.is_complex else 8)
+    print(f"{args.config} variant {args.variant} panel {args.panel}: {ms:.4f} ms/step, {b_step / ms / 1e6:.0f} GB/s, {summarize(samples)}")
 
 
 if __name__ == "__main__":
