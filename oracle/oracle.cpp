@@ -71,7 +71,7 @@ int guarded(F&& f) {
 
 // --------------------------------------------------------------- scalars ---
 // Minimal complex type with an explicit, fixed op order (the GPU kernels use
-// the same order): (a+bi)(c+di) = (ac - bd) + (ad + bc)i.
+// the same order); the SpMM accumulation is mac() below.
 struct cplx {
     double re, im;
 };
@@ -80,6 +80,17 @@ inline cplx operator-(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
 inline cplx operator*(cplx a, cplx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
 inline cplx operator*(double s, cplx a) { return {s * a.re, s * a.im}; }
 inline cplx& operator+=(cplx& a, cplx b) { a = a + b; return a; }
+// The SpMM accumulation c += v * b. Real: the reference's unfused multiply then add
+// (tiled_matrix.hpp:205 under SSE2, no FMA). Complex has no reference:
+// its accumulation is DEFINED as four fused multiply-adds in this order, which the GPU
+// kernels use too (__fma_rn); it is pinned to the real path by the 2n x 2n embedding.
+inline void mac(double& c, double v, double b) { c += v * b; }
+inline void mac(cplx& c, cplx v, cplx b) {
+    c.re = std::fma(v.re, b.re, c.re);
+    c.re = std::fma(-v.im, b.im, c.re);
+    c.im = std::fma(v.re, b.im, c.im);
+    c.im = std::fma(v.im, b.re, c.im);
+}
 
 template <class S> inline S zero();
 template <> inline double zero<double>() { return 0.0; }
@@ -281,7 +292,7 @@ void maspmm(const Tiled<S>& a, const Block<S>& b, Block<S>& c) {
                 for (index_t ii = a.colseg_ptr[jj]; ii < a.colseg_ptr[jj + 1]; ++ii) {
                     S* cseg = cdata + a.row_idx[ii] * width;
                     const S v = a.values[ii];
-                    for (index_t t = 0; t < width; ++t) cseg[t] += v * bseg[t];
+                    for (index_t t = 0; t < width; ++t) mac(cseg[t], v, bseg[t]);
                 }
             }
         }
@@ -295,7 +306,7 @@ void naive_spmm(const Csr<S>& a, const S* b, index_t k, index_t ldb, S* c, index
         for (index_t r = 0; r < a.n_rows; ++r) c[j * ldc + r] = zero<S>();
     for (index_t r = 0; r < a.n_rows; ++r)
         for (index_t kk = a.row_ptr[r]; kk < a.row_ptr[r + 1]; ++kk)
-            for (index_t j = 0; j < k; ++j) c[j * ldc + r] += a.values[kk] * b[j * ldb + a.col_idx[kk]];
+            for (index_t j = 0; j < k; ++j) mac(c[j * ldc + r], a.values[kk], b[j * ldb + a.col_idx[kk]]);
 }
 
 // ----------------------------------------------------------------- filter ---

@@ -70,10 +70,13 @@ struct CplxV {
   }
   static __device__ __forceinline__ Val zero() { return make_double2(0.0, 0.0); }
   static __device__ __forceinline__ double2 mac(double2 acc, Val v, double2 w) {
-    const double re = __dsub_rn(__dmul_rn(v.x, w.x), __dmul_rn(v.y, w.y));
-    const double im = __dadd_rn(__dmul_rn(v.x, w.y), __dmul_rn(v.y, w.x));
-    acc.x = __dadd_rn(acc.x, re);
-    acc.y = __dadd_rn(acc.y, im);
+    // complex128 has no reference implementation: its accumulation is defined
+    // as four fused multiply-adds per entry (oracle.cpp cplx mac, std::fma), half the FP64
+    // instructions of mul + add -- config 5 is FP64-issue bound
+    acc.x = __fma_rn(v.x, w.x, acc.x);
+    acc.x = __fma_rn(-v.y, w.y, acc.x);
+    acc.y = __fma_rn(v.x, w.y, acc.y);
+    acc.y = __fma_rn(v.y, w.x, acc.y);
     return acc;
   }
 };
