@@ -139,6 +139,40 @@ adp_status adp_step_device(adp_ctx* ctx, const adp_csr* a, int32_t mode, const v
                            int64_t q, int64_t row_begin, int64_t row_end, int64_t goff, double s0, double s1,
                            double s2, double s3);
 
+/* ------------------------------------------------ peer-memory halo exchange -- */
+/* Multi-GPU row partition (the reference is single-process).
+ * One process per GPU; each rank's halo-extended blocks are mapped into its neighbours
+ * (CUDA IPC over NVLink). adp_step_device_push is adp_step_device (First / Step modes)
+ * whose kernel ALSO stores every output row r in [row_lo, row_hi) to
+ * dst + (r + row_shift) * ld (ld in scalar elements of the target rows): the rows a
+ * neighbour needs land in its halo from the epilogue that computed them, with no
+ * separate collective. adp_halo_signal then publishes (release, system scope) a step
+ * count to each neighbour's counter after all prior work on the stream; adp_halo_wait
+ * queues a wait (acquire, system scope) until every local counter >= expected -- the
+ * next step's halo has landed -- failing (adp_halo_check -> ADP_ERR_NCCL) instead of
+ * hanging after timeout_ms. adp_halo_push_rows copies rows already computed (the
+ * filter's input block, narrow widths). adp_ipc_* wrap cudaIpc{Get,Open,Close}MemHandle
+ * (64-byte handles). */
+typedef struct {
+  void* dst;
+  int64_t row_lo, row_hi; /* rows of the local output block to push */
+  int64_t row_shift;      /* local row r lands at target row r + row_shift */
+  int64_t ld;             /* leading dimension of the target rows (scalar elements) */
+} adp_halo_target;
+adp_status adp_step_device_push(adp_ctx* ctx, const adp_csr* a, int32_t mode, const void* g, int64_t ld,
+                                const void* vin, const void* yin, int64_t ld_y, void* out, void* wout, int64_t ld_out,
+                                int64_t q, int64_t row_begin, int64_t row_end, int64_t goff, double s0, double s1,
+                                double s2, double s3, const adp_halo_target* targets, int32_t n_targets);
+adp_status adp_halo_push_rows(adp_ctx* ctx, const adp_csr* a, const void* src, int64_t ld, int64_t row_begin,
+                              int64_t row_end, int64_t q, const adp_halo_target* targets, int32_t n_targets);
+adp_status adp_halo_signal(adp_ctx* ctx, uint64_t* const* remote_counters, int32_t n, uint64_t value);
+adp_status adp_halo_wait(adp_ctx* ctx, const uint64_t* const* local_counters, int32_t n, uint64_t expected,
+                         uint32_t timeout_ms);
+adp_status adp_halo_check(adp_ctx* ctx);
+adp_status adp_ipc_handle(const void* dptr, void* handle_out);
+adp_status adp_ipc_open(int32_t device, const void* handle, void** dptr_out);
+adp_status adp_ipc_close(void* dptr);
+
 /* maspmm (include/adapoly/tiled_matrix.hpp:184-186): C += A B (accumulate != 0)
  * or C = A B (accumulate == 0; the reference's set_zero() + maspmm). Host
  * operands in the given layout; k = columns of B. */

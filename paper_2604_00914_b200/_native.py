@@ -67,6 +67,13 @@ class FilterInfo(C.Structure):
     ]
 
 
+class HaloTarget(C.Structure):
+    """adp_halo_target: a neighbour's rows of a halo-extended block (peer memory)."""
+
+    _fields_ = [("dst", C.c_void_p), ("row_lo", C.c_int64), ("row_hi", C.c_int64), ("row_shift", C.c_int64),
+                ("ld", C.c_int64)]
+
+
 P, I32, I64, U64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
 
 # name -> (restype, argtypes); every symbol declared in include/adp.h.
@@ -89,6 +96,14 @@ SIGNATURES = {
     "adp_filter_apply": (I32, [P, P, P, I32, D, D, I32, P, I64, I64, I64, I32, P, I64, P]),
     "adp_filter_apply_device": (I32, [P, P, P, I32, D, D, I32, P, I64, I64, I64, P, I64, P]),
     "adp_step_device": (I32, [P, P, I32, P, I64, P, P, I64, P, P, I64, I64, I64, I64, I64, D, D, D, D]),
+    "adp_step_device_push": (I32, [P, P, I32, P, I64, P, P, I64, P, P, I64, I64, I64, I64, I64, D, D, D, D, P, I32]),
+    "adp_halo_push_rows": (I32, [P, P, P, I64, I64, I64, I64, P, I32]),
+    "adp_halo_signal": (I32, [P, P, I32, U64]),
+    "adp_halo_wait": (I32, [P, P, I32, U64, C.c_uint32]),
+    "adp_halo_check": (I32, [P]),
+    "adp_ipc_handle": (I32, [P, P]),
+    "adp_ipc_open": (I32, [I32, P, P]),
+    "adp_ipc_close": (I32, [P]),
     "adp_spmm": (I32, [P, P, P, I64, I64, I64, I32, P, I64, I32]),
     "adp_spmm_device": (I32, [P, P, P, I64, I64, I64, P, I64, I32]),
     "adp_step_coeffs": (I32, [D, D, I32, P]),

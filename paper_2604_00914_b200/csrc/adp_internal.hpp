@@ -76,6 +76,7 @@ struct adp_ctx {
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;
   void* cusolver = nullptr;
+  int* halo_failed = nullptr;  // set by the halo wait kernel on timeout (adp_halo_check)
 };
 
 namespace adp {
@@ -183,6 +184,15 @@ void launch_pdl(adp_ctx* ctx, Kern kern, dim3 grid, dim3 block, size_t smem, con
 enum class StepMode : int { First = 0, Step = 1, Deg1 = 2, Spmm = 3, SpmmAcc = 4 };
 
 // One launch of the fused Clenshaw step: out = epilogue(A * G, own rows).
+// A neighbour's rows of a halo-extended buffer, mapped into this process (CUDA IPC over
+// NVLink): output row r in [lo, hi) is also stored at dst + (r + shift) * ld_b.
+constexpr int kMaxPush = 4;
+struct PushTarget {
+  char* dst;
+  int64_t lo, hi, shift;
+  uint32_t ld_b;
+};
+
 struct StepArgs {
   const adp_csr* a;
   const void* gsrc;  // gathered operand (W for Step, Y for First, X for Deg1, B for Spmm)
@@ -197,8 +207,19 @@ struct StepArgs {
   int64_t row_begin, row_end;
   int64_t goff;      // own row of out-row r inside gsrc is r + goff (0 unless halo-extended)
   double s0, s1, s2, s3;
+  const PushTarget* push = nullptr;  // First / Step: peer halo targets of the output rows (lean kernel)
+  int32_t n_push = 0;
 };
 void launch_step(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+// Halo exchange over peer memory (layout.cu): copy rows [row_begin, row_end) of src that fall in a
+// target's range to the target (then a system fence); signal: after every prior kernel on the stream,
+// store `value` (release, system scope) to each remote counter; wait: spin (acquire, system scope)
+// until every local counter >= expected (fails after ~timeout_ms rather than hanging the GPU).
+void launch_push_rows(adp_ctx* ctx, const void* src, int64_t ld_b, int64_t row_begin, int64_t row_end,
+                      int64_t row_bytes, const PushTarget* targets, int32_t n);
+void launch_halo_signal(adp_ctx* ctx, uint64_t* const* counters, int32_t n, uint64_t value);
+void launch_halo_wait(adp_ctx* ctx, const uint64_t* const* counters, int32_t n, uint64_t expected,
+                      uint32_t timeout_ms);
 
 // Layout kernels (layout.cu). Elements are 8 B (f64) or 16 B (c128).
 void launch_colmajor_to_rowmajor(adp_ctx* ctx, const void* src, int64_t n, int64_t q, int64_t lds, void* dst,

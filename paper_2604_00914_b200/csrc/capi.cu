@@ -248,6 +248,7 @@ adp_status adp_ctx_destroy(adp_ctx* ctx) {
     adp_release_dense_handles(ctx);
     for (auto& b : ctx->ws) b.release();
     ctx->sched.release();
+    if (ctx->halo_failed) cudaFree(ctx->halo_failed);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -542,6 +543,118 @@ adp_status adp_step_device(adp_ctx* ctx, const adp_csr* a, int32_t mode, const v
     s.s3 = s3;
     launch_step(ctx, static_cast<StepMode>(mode), s);
   });
+}
+
+namespace {
+std::vector<adp::PushTarget> push_targets(const adp_csr* a, const adp_halo_target* t, int32_t n) {
+  if (n < 0 || n > adp::kMaxPush) fail(ADP_ERR_CONFIG, "halo: at most 4 push targets");
+  const int64_t eb = a->dtype == ADP_C128 ? 16 : 8;
+  std::vector<adp::PushTarget> out(static_cast<size_t>(n));
+  for (int32_t i = 0; i < n; ++i) {
+    if (!t[i].dst || t[i].ld < 0 || t[i].row_lo < 0 || t[i].row_hi < t[i].row_lo)
+      fail(ADP_ERR_DIMENSION, "halo: bad push target");
+    if (t[i].ld * eb >= (int64_t{1} << 32)) fail(ADP_ERR_DIMENSION, "halo: target leading dimension too large");
+    out[i] = adp::PushTarget{static_cast<char*>(t[i].dst), t[i].row_lo, t[i].row_hi, t[i].row_shift,
+                             static_cast<uint32_t>(t[i].ld * eb)};
+  }
+  return out;
+}
+}  // namespace
+
+adp_status adp_step_device_push(adp_ctx* ctx, const adp_csr* a, int32_t mode, const void* g, int64_t ld,
+                                const void* vin, const void* yin, int64_t ld_y, void* out, void* wout, int64_t ld_out,
+                                int64_t q, int64_t row_begin, int64_t row_end, int64_t goff, double s0, double s1,
+                                double s2, double s3, const adp_halo_target* targets, int32_t n_targets) {
+  return guarded([&] {
+    if (mode != 0 && mode != 1) fail(ADP_ERR_CONFIG, "adp_step_device_push: First / Step modes only");
+    if (row_begin < 0 || row_end > a->n_rows || row_begin > row_end)
+      fail(ADP_ERR_DIMENSION, "adp_step_device_push: row range outside the operator");
+    if (q < 0 || ld < q || ld_out < q || (mode == 1 && ld_y < q))
+      fail(ADP_ERR_DIMENSION, "adp_step_device_push: leading dimension smaller than q");
+    const std::vector<adp::PushTarget> pt = push_targets(a, targets, n_targets);
+    set_device(ctx);
+    StepArgs s{};
+    s.a = a;
+    s.gsrc = g;
+    s.vin = vin;
+    s.yin = yin;
+    s.out = out;
+    s.wout = wout;
+    s.ld = ld;
+    s.ld_y = mode == 1 ? ld_y : ld;
+    s.ld_out = ld_out;
+    s.q = q;
+    s.row_begin = row_begin;
+    s.row_end = row_end;
+    s.goff = goff;
+    s.s0 = s0;
+    s.s1 = s1;
+    s.s2 = s2;
+    s.s3 = s3;
+    s.push = pt.data();
+    s.n_push = n_targets;
+    launch_step(ctx, static_cast<StepMode>(mode), s);
+  });
+}
+
+adp_status adp_halo_push_rows(adp_ctx* ctx, const adp_csr* a, const void* src, int64_t ld, int64_t row_begin,
+                              int64_t row_end, int64_t q, const adp_halo_target* targets, int32_t n_targets) {
+  return guarded([&] {
+    const std::vector<adp::PushTarget> pt = push_targets(a, targets, n_targets);
+    const int64_t eb = a->dtype == ADP_C128 ? 16 : 8;
+    set_device(ctx);
+    adp::launch_push_rows(ctx, src, ld * eb, row_begin, row_end, q * eb, pt.data(), n_targets);
+  });
+}
+
+adp_status adp_halo_signal(adp_ctx* ctx, uint64_t* const* remote_counters, int32_t n, uint64_t value) {
+  return guarded([&] {
+    set_device(ctx);
+    adp::launch_halo_signal(ctx, remote_counters, n, value);
+  });
+}
+
+adp_status adp_halo_wait(adp_ctx* ctx, const uint64_t* const* local_counters, int32_t n, uint64_t expected,
+                         uint32_t timeout_ms) {
+  return guarded([&] {
+    set_device(ctx);
+    adp::launch_halo_wait(ctx, local_counters, n, expected, timeout_ms);
+  });
+}
+
+adp_status adp_halo_check(adp_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx->halo_failed) return;
+    set_device(ctx);
+    int h = 0;
+    ADP_CUDA(cudaMemcpyAsync(&h, ctx->halo_failed, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    ADP_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h) {
+      ADP_CUDA(cudaMemsetAsync(ctx->halo_failed, 0, sizeof(int), ctx->stream));
+      fail(ADP_ERR_NCCL, "halo exchange: a neighbour did not signal within the timeout");
+    }
+  });
+}
+
+adp_status adp_ipc_handle(const void* dptr, void* handle_out) {
+  return guarded([&] {
+    cudaIpcMemHandle_t h;
+    ADP_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+    std::memcpy(handle_out, &h, sizeof(h));
+  });
+}
+
+adp_status adp_ipc_open(int32_t device, const void* handle, void** dptr_out) {
+  return guarded([&] {
+    ADP_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    ADP_CUDA(cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+adp_status adp_ipc_close(void* dptr) {
+  return guarded([&] { ADP_CUDA(cudaIpcCloseMemHandle(dptr)); });
 }
 
 adp_status adp_spmm_device(adp_ctx* ctx, const adp_csr* a, const void* db, int64_t b_rows, int64_t ldb, int64_t k,

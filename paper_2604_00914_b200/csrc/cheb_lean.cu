@@ -51,6 +51,11 @@ struct LArgs {
   int64_t g_rows;  // rows of the gathered operand (the operator's column count)
   int32_t valid;   // masked launches: vectors of the (single) panel that exist
   double s0, s1, s2, s3;
+  // Peer-memory halo push (multi-GPU row partition, First / Step modes): output rows
+  // r in [lo, hi) are also stored to dst + (r + shift) * ld_b, a neighbour's halo rows
+  // of the same buffer mapped over NVLink (CUDA IPC), by the thread that computed them.
+  PushTarget push[kMaxPush];
+  int32_t n_push;
 };
 
 struct RealL {
@@ -250,6 +255,17 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
       res = acc[c];
     }
     st_hint(ob + G * 16 * c, res, pol);
+    if constexpr (kStep || kFirst) {
+      for (int t = 0; t < p.n_push; ++t)  // uniform: 0 except on the boundary rows of a partition
+        if (r >= p.push[t].lo && r < p.push[t].hi)
+          *reinterpret_cast<double2*>(p.push[t].dst + static_cast<uint64_t>(r + p.push[t].shift) * p.push[t].ld_b +
+                                      voff + G * 16 * c) = res;
+    }
+  }
+  if constexpr (kStep || kFirst) {
+    // the peer's signal kernel follows this grid in stream order: make the remote stores
+    // performed system-wide before this thread retires
+    if (p.n_push) __threadfence_system();
   }
 }
 
@@ -1182,6 +1198,8 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   k.s1 = s.s1;
   k.s2 = s.s2;
   k.s3 = s.s3;
+  k.n_push = s.n_push;
+  for (int t = 0; t < s.n_push; ++t) k.push[t] = s.push[t];
   if (k.nrows >= (int64_t{1} << 30)) return false;
   // ragged widths: split into full-panel launches on column-offset pointers
   // panel cap (adp_ctx_set_panel): narrower panels shrink the L2 footprint of the
@@ -1202,6 +1220,7 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
       kk.yin = k.yin ? k.yin + off : nullptr;
       kk.out += off;
       kk.wout = k.wout ? k.wout + off : nullptr;
+      for (int t = 0; t < kk.n_push; ++t) kk.push[t].dst += off;
       launch_masked(ctx, mode, kk, rem, cplx, a->rp64);
       done = qv;
       break;
@@ -1221,6 +1240,7 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
     kk.yin = k.yin ? k.yin + off : nullptr;
     kk.out += off;
     kk.wout = k.wout ? k.wout + off : nullptr;
+    for (int t = 0; t < kk.n_push; ++t) kk.push[t].dst += off;
     if (cplx) {
       if (a->rp64) launch_full<CplxL, int64_t>(ctx, mode, kk, take, cap, a);
       else launch_full<CplxL, int32_t>(ctx, mode, kk, take, cap, a);
@@ -1242,6 +1262,12 @@ bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
     t.out = shift(s.out);
     t.wout = shift(s.wout);
     t.q = s.q - done * epv;
+    PushTarget pt[kMaxPush];
+    for (int i = 0; i < s.n_push; ++i) {
+      pt[i] = s.push[i];
+      pt[i].dst += off;
+    }
+    t.push = pt;
     launch_step(ctx, mode, t);
   }
   return true;

@@ -378,7 +378,28 @@ void dispatch(adp_ctx* ctx, StepMode mode, KArgs k) {
 
 }  // namespace
 
+namespace {
+void launch_step_impl(adp_ctx* ctx, StepMode mode, const StepArgs& s);
+}  // namespace
+
+// Peer-memory halo push (multi-GPU row partition): the lean kernel stores the output rows a
+// neighbour needs straight into its halo over NVLink from the epilogue that computed them.
+// Other kernels (1-3 vectors, tuning variants) compute first and copy the rows out after.
 void launch_step(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
+  if (s.n_push == 0 || s.row_end <= s.row_begin || s.q == 0) return launch_step_impl(ctx, mode, s);
+  if (mode != StepMode::First && mode != StepMode::Step) fail(ADP_ERR_CONFIG, "halo push: First / Step modes only");
+  if (s.n_push > kMaxPush) fail(ADP_ERR_CONFIG, "halo push: too many targets");
+  if (ctx->variant == 0 && ctx->tile_ch == 0 && launch_step_lean(ctx, mode, s)) return;
+  StepArgs t = s;
+  t.push = nullptr;
+  t.n_push = 0;
+  launch_step_impl(ctx, mode, t);
+  const int64_t eb = s.a->dtype == ADP_C128 ? 16 : 8;
+  launch_push_rows(ctx, s.out, s.ld_out * eb, s.row_begin, s.row_end, s.q * eb, s.push, s.n_push);
+}
+
+namespace {
+void launch_step_impl(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
   const bool cplx = a->dtype == ADP_C128;
   const int epv = cplx ? 1 : 2;
@@ -426,5 +447,6 @@ void launch_step(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
     else dispatch<RealF, int32_t>(ctx, mode, k);
   }
 }
+}  // namespace
 
 }  // namespace adp

@@ -9,6 +9,7 @@
 // both sides. Pure data movement -- bitwise exact.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <new>
@@ -257,6 +258,112 @@ void ensure_host_copy(adp_csr* a) {
   }
   a->h_values = hv;
   a->host_ready = true;
+}
+
+// ---- halo exchange over peer memory (multi-GPU row partition) ------------------------------
+namespace {
+
+struct PushSet {
+  PushTarget t[kMaxPush];
+  int32_t n;
+};
+
+// One warp per (row, target): 16-byte coalesced copies of the row into the neighbour's halo.
+__global__ void push_rows_kernel(const char* __restrict__ src, int64_t ld_b, int64_t row_begin, int64_t row_end,
+                                 int64_t row_bytes, PushSet ps) {
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  const int lane = threadIdx.x % 32;
+  bool wrote = false;
+  for (int t = 0; t < ps.n; ++t) {
+    const int64_t lo = max(row_begin, ps.t[t].lo), hi = min(row_end, ps.t[t].hi);
+    for (int64_t r = lo + (static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32); r < hi; r += warps) {
+      const int4* s4 = reinterpret_cast<const int4*>(src + r * ld_b);
+      int4* d4 = reinterpret_cast<int4*>(ps.t[t].dst + static_cast<uint64_t>(r + ps.t[t].shift) * ps.t[t].ld_b);
+      for (int64_t i = lane; i < row_bytes / 16; i += 32) d4[i] = s4[i];
+      wrote = true;
+    }
+  }
+  if (wrote) __threadfence_system();
+}
+
+struct CounterSet {
+  uint64_t* c[kMaxPush];
+  int32_t n;
+};
+
+__global__ void halo_signal_kernel(CounterSet cs, uint64_t value) {
+  // every kernel before this one on the stream has retired, and each thread that stored to a peer
+  // fenced at system scope first: the halo rows are visible to the peer before the counter moves
+  asm volatile("fence.sc.sys;\n" ::: "memory");
+  for (int i = 0; i < cs.n; ++i) asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(cs.c[i]), "l"(value) : "memory");
+}
+
+__global__ void halo_wait_kernel(CounterSet cs, uint64_t expected, uint64_t timeout_ns, int* failed) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int i = 0; i < cs.n; ++i) {
+    while (true) {
+      uint64_t v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(cs.c[i]) : "memory");
+      if (v >= expected) break;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) {  // a neighbour that never signals: fail the step, do not hang the GPU
+        *failed = 1;
+        return;
+      }
+      __nanosleep(200);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_push_rows(adp_ctx* ctx, const void* src, int64_t ld_b, int64_t row_begin, int64_t row_end,
+                      int64_t row_bytes, const PushTarget* targets, int32_t n) {
+  if (n <= 0 || row_end <= row_begin) return;
+  if (n > kMaxPush) fail(ADP_ERR_CONFIG, "halo push: too many targets");
+  if (row_bytes % 16 || ld_b % 16 || (reinterpret_cast<uintptr_t>(src) & 15u))
+    fail(ADP_ERR_DIMENSION, "halo push: rows must be 16-byte aligned");
+  PushSet ps{};
+  ps.n = n;
+  int64_t rows = 0;
+  for (int i = 0; i < n; ++i) {
+    ps.t[i] = targets[i];
+    if (ps.t[i].ld_b % 16 || (reinterpret_cast<uintptr_t>(ps.t[i].dst) & 15u))
+      fail(ADP_ERR_DIMENSION, "halo push: target rows must be 16-byte aligned");
+    rows += std::max<int64_t>(0, std::min(row_end, ps.t[i].hi) - std::max(row_begin, ps.t[i].lo));
+  }
+  if (rows == 0) return;
+  push_rows_kernel<<<grid_for(ctx, rows * 32, 256), 256, 0, ctx->stream>>>(static_cast<const char*>(src), ld_b,
+                                                                            row_begin, row_end, row_bytes, ps);
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
+}
+
+void launch_halo_signal(adp_ctx* ctx, uint64_t* const* counters, int32_t n, uint64_t value) {
+  if (n <= 0) return;
+  if (n > kMaxPush) fail(ADP_ERR_CONFIG, "halo signal: too many counters");
+  CounterSet cs{};
+  cs.n = n;
+  for (int i = 0; i < n; ++i) cs.c[i] = counters[i];
+  halo_signal_kernel<<<1, 1, 0, ctx->stream>>>(cs, value);
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
+}
+
+void launch_halo_wait(adp_ctx* ctx, const uint64_t* const* counters, int32_t n, uint64_t expected,
+                      uint32_t timeout_ms) {
+  if (n <= 0) return;
+  if (n > kMaxPush) fail(ADP_ERR_CONFIG, "halo wait: too many counters");
+  CounterSet cs{};
+  cs.n = n;
+  for (int i = 0; i < n; ++i) cs.c[i] = const_cast<uint64_t*>(counters[i]);
+  if (!ctx->halo_failed) ADP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->halo_failed), sizeof(int)));
+  halo_wait_kernel<<<1, 1, 0, ctx->stream>>>(cs, expected, static_cast<uint64_t>(timeout_ms) * 1000000ull,
+                                             ctx->halo_failed);
+  ADP_LAUNCH_CHECK();
+  ctx->launches += 1;
 }
 
 }  // namespace adp

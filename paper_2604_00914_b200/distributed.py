@@ -211,7 +211,9 @@ class CudaStepBackend:
     def upload(self, part: LocalPart):
         from .operator import DeviceCsr
 
-        return DeviceCsr(part.csr, self.ctx)
+        op = DeviceCsr(part.csr, self.ctx)
+        self._csr_for_dtype = op  # adp_halo_push_rows takes the operator for its scalar type
+        return op
 
     def alloc(self, n, q):
         ld = ((q + 1) // 2) * 2
@@ -267,3 +269,299 @@ class CudaStepBackend:
 
     def synchronize(self):
         self.torch.cuda.synchronize()
+
+    # ---- peer-memory halo (PeerHaloFilter) ----------------------------------------------------
+    def base(self, block):
+        """The full-width allocation behind a block view (what is published to the neighbours)."""
+        return block._base if block._base is not None else block
+
+    def new_counters(self, world: int):
+        c = self.torch.zeros(world, dtype=self.torch.int64, device="cuda")
+        self.torch.cuda.synchronize()
+        return c
+
+    def _halo_targets(self, targets):
+        from ._native import HaloTarget
+
+        arr = (HaloTarget * max(1, len(targets)))()
+        for i, (blk, lo, hi, shift) in enumerate(targets):
+            arr[i] = HaloTarget(blk.data_ptr(), lo, hi, shift, blk.stride(0))
+        return arr, len(targets)
+
+    def step_push(self, op, part, mode, g, vin, yin, out, wout, rows, s0, s1, s2, s3, targets):
+        import ctypes as C
+
+        from ._native import check, lib
+
+        t = self.torch
+        self.ctx.set_stream(t.cuda.current_stream())
+        lo, hi = rows
+        ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else C.c_void_p(0)  # noqa: E731
+        arr, n = self._halo_targets(targets)
+        ld_y = yin.stride(0) if yin is not None else g.stride(0)
+        check(lib().adp_step_device_push(self.ctx.h, op.h, mode, ptr(g), g.stride(0), ptr(vin), ptr(yin), ld_y,
+                                         ptr(out), ptr(wout), out.stride(0), g.shape[1], lo, hi, part.goff,
+                                         s0, s1, s2, s3, arr, n))
+
+    def push_rows(self, src, lo, hi, targets):
+        import ctypes as C
+
+        from ._native import check, lib
+
+        self.ctx.set_stream(self.torch.cuda.current_stream())
+        arr, n = self._halo_targets(targets)
+        check(lib().adp_halo_push_rows(self.ctx.h, self._csr_for_dtype.h, C.c_void_p(src.data_ptr()), src.stride(0),
+                                       lo, hi, src.shape[1], arr, n))
+
+    def signal(self, slots, value: int):
+        import ctypes as C
+
+        from ._native import check, lib
+
+        self.ctx.set_stream(self.torch.cuda.current_stream())
+        ptrs = (C.c_void_p * len(slots))(*[c.data_ptr() + 8 * i for c, i in slots])
+        check(lib().adp_halo_signal(self.ctx.h, ptrs, len(slots), int(value)))
+
+    def wait(self, slots, expected: int, timeout_ms: int):
+        import ctypes as C
+
+        from ._native import check, lib
+
+        self.ctx.set_stream(self.torch.cuda.current_stream())
+        ptrs = (C.c_void_p * len(slots))(*[c.data_ptr() + 8 * i for c, i in slots])
+        check(lib().adp_halo_wait(self.ctx.h, ptrs, len(slots), int(expected), int(timeout_ms)))
+
+    def check(self):
+        from ._native import check, lib
+
+        check(lib().adp_halo_check(self.ctx.h))
+
+
+# ---------------------------------------------------------------------------------------------
+# Peer-memory halo: the step kernel itself moves the halo (no separate collective)
+# ---------------------------------------------------------------------------------------------
+class LocalPeerDirectory:
+    """Peer buffers of ranks that live in ONE process (emulated ranks, threads): a rank's registered
+    arrays are visible to the others as they are. With a barrier (threads), publish waits for all."""
+
+    def __init__(self, barrier=None):
+        self.buffers = {}
+        self.barrier = barrier
+
+    def publish(self, rank: int, items: dict):
+        for name, t in items.items():
+            self.buffers[(rank, name)] = t
+        if self.barrier is not None:
+            self.barrier.wait()
+        return items
+
+    def lookup(self, rank: int, name: str):
+        return self.buffers[(rank, name)]
+
+
+class IpcPeerDirectory:
+    """Peer buffers across processes, one GPU each: tensors are exported with torch's CUDA IPC
+    reduction (cudaIpcGetMemHandle of the allocation + offset), exchanged with all_gather_object and
+    mapped into this process (cudaIpcOpenMemHandle: NVLink peer memory between GPUs)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.buffers = {}
+
+    def publish(self, rank: int, items: dict):
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        mine = {name: reduce_tensor(t) for name, t in items.items()}
+        world = dist.get_world_size(self.group)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (rank, mine), group=self.group)
+        for peer, exported in gathered:
+            if peer == rank:
+                continue
+            for name, (fn, args) in exported.items():
+                self.buffers[(peer, name)] = fn(*args)
+        return items
+
+    def lookup(self, rank: int, name: str):
+        return self.buffers[(rank, name)]
+
+
+class PeerHaloFilter(DistributedFilter):
+    """clenshaw_apply over a row partition with the halo exchange FUSED into the step kernel.
+
+    Each rank's halo-extended blocks (Y, W, V) and a counter array are published to its
+    neighbours (CUDA IPC: NVLink peer memory). Per degree step, on the compute stream:
+      wait   -- until every neighbour's counter reaches this step's epoch: the halo of the block
+                being gathered has landed (adp_halo_wait, acquire / system scope);
+      boundary rows (the rows that read the halo or that a neighbour needs) -- the step kernel
+                stores each output row a neighbour needs straight into that neighbour's halo of the
+                same block, from the epilogue that computed it (adp_step_device_push);
+      signal -- publish the epoch to every neighbour (adp_halo_signal, release / system scope);
+      interior rows -- local only; they overlap the neighbours' consumption of the pushed rows.
+    The signal follows ALL boundary work (also on the last step, and the next call's first push
+    waits for it), so a neighbour's next push into a block's halo waits until this rank has
+    finished gathering from it (no write-after-read race); neighbours are the union of senders
+    and receivers, so the counters are symmetric. Every rank's arithmetic is
+    the single-GPU kernel's: the gathered result is bitwise identical to one device.
+
+    ``backend`` adds to DistributedFilter's interface: step_push(op, part, mode, g, vin, yin, out,
+    wout, rows, s0..s3, targets), push_rows(src, lo, hi, targets), new_counters(world),
+    signal(counter_slots, value), wait(counter_slots, expected, timeout_ms) and check();
+    a target is (peer block, row_lo, row_hi, row_shift). ``CudaStepBackend`` is the product;
+    apply_steps() yields after every exchange point so tests can run emulated ranks in lockstep.
+    """
+
+    def __init__(self, a_global: CsrMatrix, backend, rank: int, world: int, directory, ranges=None,
+                 timeout_ms: int = 60000):
+        super().__init__(a_global, backend, rank, world, ranges)
+        self.directory = directory
+        self.timeout_ms = int(timeout_ms)
+        self.bounds = []
+        for k in range(world):
+            p0, p1 = self.ranges[k]
+            cols = a_global.col_idx[a_global.row_ptr[p0]:a_global.row_ptr[p1]]
+            self.bounds.append((p0, p1, int(min(cols.min(), p0)) if len(cols) else p0,
+                                int(max(cols.max(), p1 - 1)) if len(cols) else p1 - 1))
+        part = self.part
+        self.neighbours = sorted(set(part.sends) | set(part.recvs))
+        # interior rows: read no halo AND are sent to nobody (pushes happen in boundary launches only)
+        i0, i1 = part.interior
+        for lo, hi in part.sends.values():
+            lo, hi = lo - part.r0, hi - part.r0
+            if hi <= i0 or lo >= i1:
+                continue
+            if lo - i0 < i1 - hi:
+                i0 = max(i0, hi)
+            else:
+                i1 = min(i1, lo)
+        self.inner = (i0, max(i0, i1))
+        self.q = None
+        self.epoch = 0
+
+    def _prepare(self, q: int):
+        """Blocks of width q and the counters, published to the neighbours (collective when over IPC)."""
+        if self.q == q:
+            return
+        be, part = self.backend, self.part
+        self.bufs = {name: be.alloc(part.n_ext, q) for name in ("y", "a", "b")}
+        self.counters = be.new_counters(self.world)
+        items = {f"buf_{k}": be.base(v) for k, v in self.bufs.items()}
+        items["counters"] = self.counters
+        self.directory.publish(self.rank, items)
+        self.peer_bufs = self.peer_counters = None  # resolved after every rank has published
+        self.q = q
+        self.epoch = 0
+
+    def _resolve(self):
+        if self.peer_bufs is None:
+            self.peer_bufs = {p: {k: self.directory.lookup(p, f"buf_{k}") for k in self.bufs} for p in self.neighbours}
+            self.peer_counters = {p: self.directory.lookup(p, "counters") for p in self.neighbours}
+
+    def _targets(self, name: str):
+        """My rows each neighbour needs -> its rows of block `name`: (block, lo, hi, shift) in my local rows."""
+        part = self.part
+        return [(self.peer_bufs[peer][name], lo - part.r0, hi - part.r0, part.r0 - self.bounds[peer][2])
+                for peer, (lo, hi) in part.sends.items()]
+
+    def _signal(self):
+        self.epoch += 1
+        self.backend.signal([(self.peer_counters[p], self.rank) for p in self.neighbours], self.epoch)
+
+    def _wait(self):
+        self.backend.wait([(self.counters, p) for p in self.neighbours], self.epoch, self.timeout_ms)
+
+    def _step(self, mode, g, vin, yin, out, wout, rows, s, push_name):
+        if rows[1] <= rows[0]:
+            return
+        if push_name is None or not self.part.sends:
+            return self.backend.step(self.op, self.part, mode, g, vin, yin, out, wout, rows, *s)
+        self.backend.step_push(self.op, self.part, mode, g, vin, yin, out, wout, rows, *s, self._targets(push_name))
+
+    def _run_fused(self, mode, g, vin, yin, out, wout, s, push_name):
+        part = self.part
+        i0, i1 = self.inner
+        if self.neighbours:
+            self._wait()
+        for rows in ((0, i0), (i1, part.n_local)):
+            self._step(mode, g, vin, yin, out, wout, rows, s, push_name)
+        if self.neighbours:  # after the last step too: "done gathering from my halos" for the next call
+            self._signal()
+        self._step(mode, g, vin, yin, out, wout, (i0, i1), s, None)
+
+    def _push_input(self, x_local, name: str):
+        """Own rows of the filter's input into the neighbours' halo of block `name` (rows already computed).
+        Waits first for the neighbours' last signal of the previous call: they no longer read that halo."""
+        if self.neighbours and self.epoch > 0:
+            self._wait()
+        if self.part.sends:
+            self.backend.push_rows(x_local, 0, self.part.n_local, self._targets(name))
+        if self.neighbours:
+            self._signal()
+
+    def apply_steps(self, coeffs, l1, l2, x_local, degree: int):
+        """Generator form of apply(): yields after each exchange point; its return value is the result."""
+        be, part = self.backend, self.part
+        deg = int(degree)
+        while deg > 0 and coeffs[deg] == 0.0:  # cheb_filter.cpp:141-142
+            deg -= 1
+        q = be.width(x_local)
+        if deg == 0:
+            return be.scale(x_local, float(coeffs[0]))
+        fresh = self.q != q
+        self._prepare(q)
+        if fresh:
+            yield  # every rank publishes its blocks before anyone maps a neighbour's
+        self._resolve()
+        g0, g1 = part.goff, part.goff + part.n_local
+        y_ext, a_buf, b_buf = self.bufs["y"], self.bufs["a"], self.bufs["b"]
+        if deg == 1:
+            be.copy_rows(be.rows(a_buf, g0, g1), x_local)
+            self._push_input(x_local, "a")
+            yield
+            out = be.alloc(part.n_local, q)
+            self._run_fused(DEG1, a_buf, None, None, out, None, (coeffs[0], coeffs[1], l1, l2), None)
+            be.check()
+            return out
+        be.copy_rows(be.rows(y_ext, g0, g1), x_local)
+        self._push_input(x_local, "y")
+        yield
+        # w = c_d y -> a ; v -> b (pushed: the next step gathers b)
+        self._run_fused(FIRST, y_ext, None, None, be.rows(b_buf, g0, g1), be.rows(a_buf, g0, g1),
+                        (2.0 * l1, 2.0 * l2 + coeffs[deg - 1] / coeffs[deg], coeffs[deg], 0.0), "b")
+        yield
+        cur_w, cur_v, names = b_buf, a_buf, ("b", "a")
+        for j in range(deg - 2, 0, -1):
+            v_rows = be.rows(cur_v, g0, g1)
+            self._run_fused(STEP, cur_w, v_rows, x_local, v_rows, None, (2.0 * l1, 2.0 * l2, coeffs[j], 0.0), names[1])
+            yield
+            cur_w, cur_v, names = cur_v, cur_w, (names[1], names[0])
+        out = be.alloc(part.n_local, q)
+        self._run_fused(STEP, cur_w, be.rows(cur_v, g0, g1), x_local, out, None, (l1, l2, coeffs[0], 0.0), None)
+        be.check()
+        return out
+
+    def apply(self, coeffs, l1, l2, x_local, degree: int):
+        gen = self.apply_steps(coeffs, l1, l2, x_local, degree)
+        while True:
+            try:
+                next(gen)
+            except StopIteration as stop:
+                return stop.value
+
+
+def run_lockstep(filters, xs, coeffs, l1, l2, degree):
+    """Drive several ranks' PeerHaloFilter.apply_steps round-robin, one exchange point at a time, on
+    ONE stream: every wait is already satisfied when it is queued (its signal was queued earlier),
+    so no kernel ever waits on a concurrently running one. Returns each rank's result."""
+    gens = [f.apply_steps(coeffs, l1, l2, x, degree) for f, x in zip(filters, xs)]
+    out = [None] * len(gens)
+    live = set(range(len(gens)))
+    while live:
+        for k in sorted(live):
+            try:
+                next(gens[k])
+            except StopIteration as stop:
+                out[k] = stop.value
+                live.discard(k)
+    return out

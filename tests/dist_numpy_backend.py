@@ -7,12 +7,25 @@ DistributedFilter driver on CPU is bitwise comparable with the single-process
 oracle. The halo exchange goes through torch.distributed (gloo) exactly as the
 CUDA backend's goes through NCCL.
 """
+import random
+import time
+
 import numpy as np
 
 FIRST, STEP, DEG1, SPMM, SPMM_ACC = 0, 1, 2, 3, 4
 
 
 class NumpyStepBackend:
+    def __init__(self, jitter: float = 0.0, seed: int = 0):
+        # jitter: random sleeps (seconds) around the exchange points, so concurrent ranks (threads)
+        # interleave in many orders -- a protocol race would show up as a wrong (non-bitwise) result
+        self.jitter = jitter
+        self.rng = random.Random(seed)
+
+    def _jit(self):
+        if self.jitter:
+            time.sleep(self.rng.random() * self.jitter)
+
     def upload(self, part):
         return part.csr
 
@@ -77,4 +90,43 @@ class NumpyStepBackend:
             w.wait()
 
     def synchronize(self):
+        pass
+
+    # ---- peer-memory halo (PeerHaloFilter), ranks as threads of one process --------------------
+    def base(self, block):
+        return block
+
+    def new_counters(self, world):
+        return np.zeros(world, np.int64)
+
+    def step_push(self, op, part, mode, g, vin, yin, out, wout, rows, s0, s1, s2, s3, targets):
+        lo, hi = rows
+        self.step(op, part, mode, g, vin, yin, out, wout, rows, s0, s1, s2, s3)
+        self._jit()
+        for blk, tlo, thi, shift in targets:  # the kernel's epilogue stores: the rows it computed
+            a, b = max(lo, tlo), min(hi, thi)
+            if a < b:
+                blk[a + shift:b + shift] = out[a:b]
+
+    def push_rows(self, src, lo, hi, targets):
+        for blk, tlo, thi, shift in targets:
+            a, b = max(lo, tlo), min(hi, thi)
+            if a < b:
+                blk[a + shift:b + shift] = src[a:b]
+
+    def signal(self, slots, value):
+        self._jit()
+        for c, i in slots:
+            c[i] = value
+
+    def wait(self, slots, expected, timeout_ms):
+        t0 = time.time()
+        for c, i in slots:
+            while c[i] < expected:
+                if time.time() - t0 > timeout_ms / 1e3:
+                    raise TimeoutError("halo wait timed out")
+                time.sleep(1e-5)
+        self._jit()
+
+    def check(self):
         pass

@@ -118,3 +118,66 @@ def test_partition_and_schedule():
         cols = p.csr.col_idx + p.cmin
         sel = (rows >= i0) & (rows < i1)
         assert np.all((cols[sel] >= p.r0) & (cols[sel] < p.r1))
+
+
+# ----------------------------------------------------------- peer-memory halo protocol ---
+# PeerHaloFilter moves the halo inside the step (push into the neighbour's block + release
+# counter; acquire wait before gathering). Here the ranks are THREADS of one process sharing
+# numpy blocks, with random sleeps around every exchange point, so they really run concurrently
+# and interleave in many orders: a missing wait, an early signal or a write-after-read race on
+# a block's halo would make the result differ from the oracle. Two applies back to back check
+# that the next filter call cannot overwrite a halo the previous one is still reading.
+@pytest.mark.parametrize("kind,world,degree,q,seed", [
+    ("lap", 2, 9, 6, 0), ("lap", 3, 25, 5, 1), ("lap", 4, 6, 3, 6), ("27pt", 2, 12, 3, 2), ("band", 3, 7, 2, 3),
+    ("band", 2, 2, 3, 4), ("lap", 2, 1, 4, 5)])
+def test_peer_halo_filter_threads_bitwise(orc, kind, world, degree, q, seed):
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from dist_numpy_backend import NumpyStepBackend
+    from paper_2604_00914_b200.distributed import LocalPeerDirectory, PeerHaloFilter
+
+    a = _matrix(kind)
+    n = a.n_rows
+    ev = np.linalg.eigvalsh(a.to_dense())
+    f = orc.build_filter(ev[n // 3], ev[n // 2], (ev[0] - 0.1, ev[-1] + 0.1), max(degree, 1), 0.5)
+    xs = [orc.fill_gaussian(n, q, 9 + i, 0) for i in range(2)]
+    directory = LocalPeerDirectory(threading.Barrier(world))
+    filters = [PeerHaloFilter(a, NumpyStepBackend(jitter=0.002, seed=100 * seed + k), k, world, directory,
+                              timeout_ms=60000) for k in range(world)]
+
+    def rank_main(k):
+        r0, r1 = filters[k].ranges[k]
+        return [filters[k].apply(f.coeffs, f.l1, f.l2, np.ascontiguousarray(x[r0:r1]), degree) for x in xs]
+
+    with ThreadPoolExecutor(world) as ex:
+        res = list(ex.map(rank_main, range(world)))
+    oa = orc.Csr(n, n, a.row_ptr, a.col_idx, a.values)
+    for i, x in enumerate(xs):
+        want = orc.clenshaw_apply(f, orc.Tiled(oa, 256, 64), x, degree)
+        got = np.concatenate([res[k][i] for k in range(world)])
+        assert np.array_equal(got, want), (kind, world, i)
+
+
+def test_peer_halo_boundary_covers_sends_and_halo_reads():
+    # the launches that push (boundary) must contain every row a neighbour needs and every row that
+    # reads the halo; the interior must do neither (the write-after-read argument relies on it)
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from dist_numpy_backend import NumpyStepBackend
+    from paper_2604_00914_b200.distributed import LocalPeerDirectory, PeerHaloFilter
+
+    for kind, world in (("lap", 3), ("27pt", 2), ("band", 3)):
+        a = _matrix(kind)
+        for k in range(world):
+            pf = PeerHaloFilter(a, NumpyStepBackend(), k, world, LocalPeerDirectory())
+            p = pf.part
+            i0, i1 = pf.inner
+            rows = np.repeat(np.arange(p.n_local), np.diff(p.csr.row_ptr))
+            cols = p.csr.col_idx + p.cmin
+            sel = (rows >= i0) & (rows < i1)
+            assert np.all((cols[sel] >= p.r0) & (cols[sel] < p.r1))
+            for lo, hi in p.sends.values():
+                assert hi - p.r0 <= i0 or lo - p.r0 >= i1
+            assert set(pf.neighbours) == set(p.sends) | set(p.recvs)

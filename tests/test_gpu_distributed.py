@@ -104,3 +104,40 @@ def test_emulated_ranks_bitwise(orc, world, degree, q):
 
     got = np.concatenate(run_ranks(a, world, fn))
     assert np.array_equal(got, want)
+
+
+# ------------------------------------------------ halo pushed by the step kernel (peer memory) ---
+# PeerHaloFilter with the product backend: the lean kernel's epilogue stores the rows a neighbour
+# needs straight into the neighbour's block (here: another emulated rank's tensor on the same
+# device; across GPUs the same store goes over NVLink to a CUDA-IPC mapping), and the 1-thread
+# signal / wait kernels order the exchange. The emulated ranks share ONE stream and run in
+# lockstep (run_lockstep): every wait is queued after the signal it waits for, so no kernel
+# waits on a concurrently running one. Bitwise equal to the single-device filter; two calls
+# back to back, ragged and narrow widths (narrow ones push with the copy kernel).
+@pytest.mark.parametrize("world,degree,q,kind", [(2, 12, 64, "lap"), (3, 7, 6, "lap"), (2, 1, 130, "lap"),
+                                                  (4, 20, 256, "lap"), (2, 9, 2, "lap"), (3, 5, 100, "27pt")])
+def test_peer_halo_lockstep_bitwise(orc, world, degree, q, kind):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_00914_b200 import configs
+    from paper_2604_00914_b200.distributed import CudaStepBackend, LocalPeerDirectory, PeerHaloFilter, run_lockstep
+
+    a = configs.laplacian7_potential(20, -2.0, 2.0, seed=1) if kind == "lap" else configs.dft_like_27pt(12, 4, 2)
+    n = a.n_rows
+    f = adp.build_filter(5.9, 6.1, (-2.0, 14.0), 40, 0.5)
+    ctx = adp.Context(0)
+    ctx.set_stream(torch.cuda.current_stream())
+    directory = LocalPeerDirectory()
+    filters = [PeerHaloFilter(a, CudaStepBackend(ctx), k, world, directory, timeout_ms=5000) for k in range(world)]
+    launches0 = ctx.launch_count
+    for seed in (3, 4):
+        x = orc.fill_gaussian(n, q, seed, 0)
+        want = adp.clenshaw_apply(f, adp.DeviceCsr(a, ctx), x, degree)
+        xs = []
+        for k in range(world):
+            r0, r1 = filters[k].ranges[k]
+            xs.append(torch.from_numpy(np.ascontiguousarray(x[r0:r1])).cuda())
+        outs = run_lockstep(filters, xs, f.coeffs, f.l1, f.l2, degree)
+        got = np.concatenate([o.cpu().numpy() for o in outs])
+        assert np.array_equal(got, want), seed
+    assert ctx.launch_count > launches0
