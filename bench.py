@@ -56,6 +56,9 @@ def parse_args():
     p.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve (second half of the metric)")
     p.add_argument("--panel", type=int, default=0)
     p.add_argument("--variant", type=int, default=0)
+    p.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
+                   help="N > 1: halo rows stored by the step kernel into the neighbour's block over NVLink "
+                        "(p2p, CUDA IPC) or exchanged with NCCL send/recv between steps")
     return p.parse_args()
 
 
@@ -391,25 +394,49 @@ def run_ours(args):
 
 
 def run_distributed(args, adp, cfg, a, f, degree, rank, world, device):
-    """N > 1: the filter row-partitioned over the ranks (strong scaling: the operator is fixed),
-    halo rows exchanged per degree step over NCCL while interior rows compute
-    (paper_2604_00914_b200/distributed.py)."""
+    """N > 1: the filter row-partitioned over the ranks (strong scaling: the operator is fixed).
+    Default (--halo p2p): the step kernel stores the rows each neighbour needs straight into the
+    neighbour's block over NVLink (CUDA IPC mappings) and publishes a counter; the neighbour's next
+    step waits on it (PeerHaloFilter). --halo nccl: NCCL send/recv of the halo rows between steps
+    while interior rows compute (DistributedFilter). If the peer-memory setup fails on a box, the
+    NCCL exchange is used and the JSON line says so (paper_2604_00914_b200/distributed.py)."""
     import torch
     import torch.distributed as dist
 
-    from paper_2604_00914_b200.distributed import CudaStepBackend, DistributedFilter
+    from paper_2604_00914_b200.distributed import CudaStepBackend, DistributedFilter, IpcPeerDirectory, PeerHaloFilter
 
     n, nnz, q = a.n_rows, a.nnz, cfg.q
     ctx = adp.Context(device)
     be = CudaStepBackend(ctx)
-    df = DistributedFilter(a, be, rank, world)
-    r0, r1 = df.ranges[rank]
+    ranges = None
     g = torch.Generator(device="cuda").manual_seed(rank)
-    x = torch.randn(r1 - r0, q, dtype=torch.float64, device="cuda", generator=g)
 
     def barrier():
         dist.barrier()
         torch.cuda.synchronize()
+
+    halo = args.halo
+    note = None
+    df = None
+    if halo == "p2p":
+        try:
+            df = PeerHaloFilter(a, be, rank, world, IpcPeerDirectory(), timeout_ms=30000)
+            r0, r1 = df.ranges[rank]
+            x = torch.randn(r1 - r0, q, dtype=torch.float64, device="cuda", generator=g)
+            df.apply(f.coeffs, f.l1, f.l2, x, min(degree, 3))
+            torch.cuda.synchronize()
+            ok = torch.tensor([1], device="cuda")
+        except Exception as e:  # pragma: no cover - depends on the box's peer access
+            note = f"peer-memory halo unavailable ({type(e).__name__}: {str(e)[:160]}); NCCL exchange used"
+            ok = torch.tensor([0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            halo, df = "nccl", None
+            note = note or "peer-memory halo failed on another rank; NCCL exchange used"
+    if df is None:
+        df = DistributedFilter(a, be, rank, world, ranges)
+    r0, r1 = df.ranges[rank]
+    x = torch.randn(r1 - r0, q, dtype=torch.float64, device="cuda", generator=g)
 
     for _ in range(args.warmup):
         df.apply(f.coeffs, f.l1, f.l2, x, degree)
@@ -460,7 +487,11 @@ def run_distributed(args, adp, cfg, a, f, degree, rank, world, device):
             "config": {"workload": f"{args.config}: {cfg.description}; clenshaw_apply degree {degree}, "
                                    f"rows partitioned over {world} GPUs, halo exchange per degree step",
                        "n": n, "nnz": nnz, "q": q, "degree": degree, "bytes_per_step": bytes_call,
-                       "l2": "inputs larger than L2", "parallelism": f"row-partition x{world} (NCCL halo)"},
+                       "l2": "inputs larger than L2",
+                       "parallelism": f"row-partition x{world} ("
+                                      + ("halo stored by the step kernel into peer memory over NVLink" if halo == "p2p"
+                                         else "NCCL halo send/recv") + ")",
+                       "halo": halo, **({"halo_note": note} if note else {})},
             "pct_of_hbm_peak_per_gpu": round(100.0 * value / world / peak, 2),
             "gpu_launches": ctx.launch_count - launches0, "clocks": clk, "e2e": e2e, "cpu_baseline": None,
         }

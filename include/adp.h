@@ -163,7 +163,7 @@ adp_status adp_step_device_push(adp_ctx* ctx, const adp_csr* a, int32_t mode, co
                                 const void* vin, const void* yin, int64_t ld_y, void* out, void* wout, int64_t ld_out,
                                 int64_t q, int64_t row_begin, int64_t row_end, int64_t goff, double s0, double s1,
                                 double s2, double s3, const adp_halo_target* targets, int32_t n_targets);
-adp_status adp_halo_push_rows(adp_ctx* ctx, const adp_csr* a, const void* src, int64_t ld, int64_t row_begin,
+adp_status adp_halo_push_rows(adp_ctx* ctx, adp_dtype dtype, const void* src, int64_t ld, int64_t row_begin,
                               int64_t row_end, int64_t q, const adp_halo_target* targets, int32_t n_targets);
 adp_status adp_halo_signal(adp_ctx* ctx, uint64_t* const* remote_counters, int32_t n, uint64_t value);
 adp_status adp_halo_wait(adp_ctx* ctx, const uint64_t* const* local_counters, int32_t n, uint64_t expected,

@@ -97,7 +97,7 @@ SIGNATURES = {
     "adp_filter_apply_device": (I32, [P, P, P, I32, D, D, I32, P, I64, I64, I64, P, I64, P]),
     "adp_step_device": (I32, [P, P, I32, P, I64, P, P, I64, P, P, I64, I64, I64, I64, I64, D, D, D, D]),
     "adp_step_device_push": (I32, [P, P, I32, P, I64, P, P, I64, P, P, I64, I64, I64, I64, I64, D, D, D, D, P, I32]),
-    "adp_halo_push_rows": (I32, [P, P, P, I64, I64, I64, I64, P, I32]),
+    "adp_halo_push_rows": (I32, [P, I32, P, I64, I64, I64, I64, P, I32]),
     "adp_halo_signal": (I32, [P, P, I32, U64]),
     "adp_halo_wait": (I32, [P, P, I32, U64, C.c_uint32]),
     "adp_halo_check": (I32, [P]),

@@ -546,9 +546,8 @@ adp_status adp_step_device(adp_ctx* ctx, const adp_csr* a, int32_t mode, const v
 }
 
 namespace {
-std::vector<adp::PushTarget> push_targets(const adp_csr* a, const adp_halo_target* t, int32_t n) {
+std::vector<adp::PushTarget> push_targets(int64_t eb, const adp_halo_target* t, int32_t n) {
   if (n < 0 || n > adp::kMaxPush) fail(ADP_ERR_CONFIG, "halo: at most 4 push targets");
-  const int64_t eb = a->dtype == ADP_C128 ? 16 : 8;
   std::vector<adp::PushTarget> out(static_cast<size_t>(n));
   for (int32_t i = 0; i < n; ++i) {
     if (!t[i].dst || t[i].ld < 0 || t[i].row_lo < 0 || t[i].row_hi < t[i].row_lo)
@@ -571,7 +570,7 @@ adp_status adp_step_device_push(adp_ctx* ctx, const adp_csr* a, int32_t mode, co
       fail(ADP_ERR_DIMENSION, "adp_step_device_push: row range outside the operator");
     if (q < 0 || ld < q || ld_out < q || (mode == 1 && ld_y < q))
       fail(ADP_ERR_DIMENSION, "adp_step_device_push: leading dimension smaller than q");
-    const std::vector<adp::PushTarget> pt = push_targets(a, targets, n_targets);
+    const std::vector<adp::PushTarget> pt = push_targets(a->dtype == ADP_C128 ? 16 : 8, targets, n_targets);
     set_device(ctx);
     StepArgs s{};
     s.a = a;
@@ -597,11 +596,12 @@ adp_status adp_step_device_push(adp_ctx* ctx, const adp_csr* a, int32_t mode, co
   });
 }
 
-adp_status adp_halo_push_rows(adp_ctx* ctx, const adp_csr* a, const void* src, int64_t ld, int64_t row_begin,
+adp_status adp_halo_push_rows(adp_ctx* ctx, adp_dtype dtype, const void* src, int64_t ld, int64_t row_begin,
                               int64_t row_end, int64_t q, const adp_halo_target* targets, int32_t n_targets) {
   return guarded([&] {
-    const std::vector<adp::PushTarget> pt = push_targets(a, targets, n_targets);
-    const int64_t eb = a->dtype == ADP_C128 ? 16 : 8;
+    if (dtype != ADP_F64 && dtype != ADP_C128) fail(ADP_ERR_CONFIG, "adp_halo_push_rows: unknown dtype");
+    const int64_t eb = dtype == ADP_C128 ? 16 : 8;
+    const std::vector<adp::PushTarget> pt = push_targets(eb, targets, n_targets);
     set_device(ctx);
     adp::launch_push_rows(ctx, src, ld * eb, row_begin, row_end, q * eb, pt.data(), n_targets);
   });

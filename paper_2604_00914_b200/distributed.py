@@ -211,9 +211,7 @@ class CudaStepBackend:
     def upload(self, part: LocalPart):
         from .operator import DeviceCsr
 
-        op = DeviceCsr(part.csr, self.ctx)
-        self._csr_for_dtype = op  # adp_halo_push_rows takes the operator for its scalar type
-        return op
+        return DeviceCsr(part.csr, self.ctx)
 
     def alloc(self, n, q):
         ld = ((q + 1) // 2) * 2
@@ -310,8 +308,11 @@ class CudaStepBackend:
 
         self.ctx.set_stream(self.torch.cuda.current_stream())
         arr, n = self._halo_targets(targets)
-        check(lib().adp_halo_push_rows(self.ctx.h, self._csr_for_dtype.h, C.c_void_p(src.data_ptr()), src.stride(0),
-                                       lo, hi, src.shape[1], arr, n))
+        from ._native import ADP_C128, ADP_F64
+
+        dt = ADP_C128 if src.is_complex() else ADP_F64
+        check(lib().adp_halo_push_rows(self.ctx.h, dt, C.c_void_p(src.data_ptr()), src.stride(0), lo, hi, src.shape[1],
+                                       arr, n))
 
     def signal(self, slots, value: int):
         import ctypes as C

@@ -141,3 +141,63 @@ def test_peer_halo_lockstep_bitwise(orc, world, degree, q, kind):
         got = np.concatenate([o.cpu().numpy() for o in outs])
         assert np.array_equal(got, want), seed
     assert ctx.launch_count > launches0
+
+
+def _ipc_worker(rank, port, out_path):
+    import os
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_00914_b200 as adp
+    from paper_2604_00914_b200.distributed import CudaStepBackend, IpcPeerDirectory
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    torch.cuda.set_device(0)
+    ctx = adp.Context(0)
+    be = CudaStepBackend(ctx)
+    q, n_ext = 40, 64
+    blk = be.alloc(n_ext, q)
+    counters = be.new_counters(2)
+    d = IpcPeerDirectory()
+    d.publish(rank, {"blk": be.base(blk), "counters": counters})
+    peer = 1 - rank
+    pblk, pcnt = d.lookup(peer, "blk"), d.lookup(peer, "counters")
+    src = torch.arange(10 * q, dtype=torch.float64, device="cuda").reshape(10, q) + 1000.0 * rank
+    # rows 3..7 of mine land at the peer's rows 3 + 20 + rank ... (shift 20 + rank); then the counter
+    be.push_rows(src, 0, 10, [(pblk, 3, 8, 20 + rank)])
+    be.signal([(pcnt, rank)], 7 + rank)
+    torch.cuda.synchronize()
+    dist.barrier()  # host-side: no kernel waits on the other process
+    ok_rows = torch.equal(blk[3 + 20 + peer:8 + 20 + peer], (torch.arange(10 * q, dtype=torch.float64, device="cuda")
+                                                           .reshape(10, q) + 1000.0 * peer)[3:8])
+    untouched = float(blk.abs().sum()) == float(blk[3 + 20 + peer:8 + 20 + peer].abs().sum())
+    with open(f"{out_path}.{rank}", "w") as fh:
+        fh.write(f"{int(ok_rows)} {int(untouched)} {int(counters[peer])}\n")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_ipc_directory_push_and_signal_two_processes(tmp_path):
+    # the cross-process half of the peer-memory halo: torch CUDA IPC export / import of a block and
+    # the counters (IpcPeerDirectory), rows stored into the other process's block at the right
+    # shift, the counter value published. Two processes on the one device; neither kernel waits.
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = str(tmp_path / "ipc")
+    mp.start_processes(_ipc_worker, args=(port, out), nprocs=2, join=True, start_method="spawn")
+    for rank in range(2):
+        ok_rows, untouched, cnt = open(f"{out}.{rank}").read().split()
+        assert ok_rows == "1" and untouched == "1" and int(cnt) == 7 + (1 - rank)
