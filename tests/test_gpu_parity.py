@@ -58,7 +58,7 @@ def test_golden_fixtures(ctx, golden_dir):
 
 
 # --------------------------------------------- reference hot-path test cases ---
-@pytest.mark.parametrize("q", [1, 2, 3, 5, 6, 8, 16, 17, 30, 33, 64, 65, 128, 130, 256, 384, 520, 1024])
+@pytest.mark.parametrize("q", [1, 2, 3, 5, 6, 8, 16, 17, 30, 33, 64, 65, 128, 130, 256, 266, 290, 362, 384, 520, 1024])
 def test_clenshaw_bitwise_widths(ctx, orc, q):
     # random_symmetric(80, 0.1, 31) -- the matrix of test_cheb_filter.cpp:225-240
     a = orc.random_symmetric(80, 0.1, 31)
@@ -219,7 +219,7 @@ def random_hermitian(n, density, seed):
 
 
 def test_complex_bitwise_vs_oracle(ctx, orc):
-    for n, q in [(90, 3), (150, 16), (200, 40), (256, 130)]:
+    for n, q in [(90, 3), (150, 16), (200, 40), (256, 130), (210, 150), (180, 200)]:
         h = random_hermitian(n, 0.05, n)
         oh = orc.Csr(h.n_rows, h.n_cols, h.row_ptr, h.col_idx, h.values)
         ev = np.linalg.eigvalsh(h.to_dense())
