@@ -255,17 +255,23 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_lean_kernel(const LArgs p
       res = acc[c];
     }
     st_hint(ob + G * 16 * c, res, pol);
-    if constexpr (kStep || kFirst) {
-      for (int t = 0; t < p.n_push; ++t)  // uniform: 0 except on the boundary rows of a partition
-        if (r >= p.push[t].lo && r < p.push[t].hi)
-          *reinterpret_cast<double2*>(p.push[t].dst + static_cast<uint64_t>(r + p.push[t].shift) * p.push[t].ld_b +
-                                      voff + G * 16 * c) = res;
-    }
+    acc[c] = res;  // kept for the halo push below
   }
   if constexpr (kStep || kFirst) {
-    // the peer's signal kernel follows this grid in stream order: make the remote stores
-    // performed system-wide before this thread retires
-    if (p.n_push) __threadfence_system();
+    // peer-memory halo: rows a neighbour needs also go straight into its block (one uniform
+    // branch per row when not partitioned); then a system fence -- the peer's signal kernel
+    // follows this grid in stream order, so the remote stores are performed before it runs
+    if (p.n_push) {
+      for (int t = 0; t < p.n_push; ++t) {
+        if (r >= p.push[t].lo && r < p.push[t].hi) {
+          char* dst = p.push[t].dst + static_cast<uint64_t>(r + p.push[t].shift) * p.push[t].ld_b + voff;
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+            if (ok[c]) *reinterpret_cast<double2*>(dst + G * 16 * c) = acc[c];
+        }
+      }
+      __threadfence_system();
+    }
   }
 }
 
