@@ -282,7 +282,7 @@ adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
   return guarded([&] {
     // 0 auto; 1-7 one-row kernel; 11-15 pipelined row kernel; 21-24 union; 31-33 deep batches; 41-46 segments
     if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) ||
-        (variant > 24 && variant < 31) || (variant > 33 && variant < 41) || (variant > 46 && variant < 51) ||
+        (variant > 24 && variant < 31) || (variant > 33 && variant < 40) || (variant > 49 && variant < 51) ||
         (variant > 56 && variant < 61) || (variant > 66 && variant < 71) || (variant > 76 && variant < 81) ||
         (variant > 98 && variant < 101) || variant > 108)
       fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");

@@ -1117,6 +1117,10 @@ void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_
     case 44: if (qv % 64 == 0 && launch_seg<F, 2, 2, 4, 3>(ctx, mode, k, qv, a)) return; break;
     case 45: if (qv % 32 == 0 && launch_seg<F, 1, 4, 4, 4>(ctx, mode, k, qv, a)) return; break;
     case 46: if (qv % 128 == 0 && launch_seg<F, 4, 4, 1, 1>(ctx, mode, k, qv, a)) return; break;
+    case 47: if (qv % 128 == 0 && launch_seg<F, 4, 4, 1, 2>(ctx, mode, k, qv, a)) return; break;
+    case 48: if (qv % 64 == 0 && launch_seg<F, 2, 4, 2, 3>(ctx, mode, k, qv, a)) return; break;
+    case 49: if (qv % 64 == 0 && launch_seg<F, 2, 4, 1, 4>(ctx, mode, k, qv, a)) return; break;
+    case 40: if (qv % 128 == 0 && launch_seg<F, 4, 3, 1, 2>(ctx, mode, k, qv, a)) return; break;
     // lane-parallel metadata (tuning variants 51-56)
     case 51: if (qv % 128 == 0) return launch_lean2<F, 4, 2, RP, 2>(ctx, mode, k, qv); break;
     case 52: if (qv % 128 == 0) return launch_lean2<F, 4, 4, RP, 2>(ctx, mode, k, qv); break;
