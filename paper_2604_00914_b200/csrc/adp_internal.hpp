@@ -138,6 +138,24 @@ struct LinePlan {
   void* d_runs = nullptr;     // int4[n_runs]: {first column - r0, entry index, length, 0}
   ~LinePlan();
 };
+// Blocks of L = ly * lz lines of R consecutive rows (line l at r0 + off[l]) for the
+// cube kernel (cheb_cube.cu): the union of the lines' column runs per shifted pattern.
+constexpr int64_t kCubeValueSlot = 2048;  // bytes of shared memory per warp for a block's fp64 values (x2 complex)
+struct CubePlan {
+  int R = 0, ly = 0, lz = 0, mm = 0;
+  bool valid = false;         // strides found and blocks built
+  int64_t sy = 0, sz = 0;     // line strides derived from the dominant pattern
+  int32_t off[8] = {};
+  int64_t n_blocks = 0, n_regular = 0, n_rem = 0, n_patterns = 0, n_items = 0;
+  double regular_rows_frac = 0.0;
+  void* d_blk = nullptr;      // int4[n_blocks]: {r0, pattern, value offset lo, hi} (pattern -1: row by row, -2: r0 indexes the remainder list)
+  void* d_pat_ptr = nullptr;  // int32[n_patterns+1]: items of each pattern
+  void* d_pat_nv = nullptr;   // int32[n_patterns]: values per block of each pattern
+  void* d_items = nullptr;    // int4[n_items]: {start - r0, length, line mask, 0}
+  void* d_rem = nullptr;      // int32[n_rem]: rows outside every full block
+  void* d_vals = nullptr;     // the regular blocks' values in kernel consumption order (item, line, row, position)
+  ~CubePlan();
+};
 }  // namespace adp
 
 struct adp_csr {
@@ -158,6 +176,7 @@ struct adp_csr {
   std::vector<std::unique_ptr<adp::Segments>> segments;
   std::vector<std::unique_ptr<adp::PairPlan>> pair_plans;
   std::vector<std::unique_ptr<adp::LinePlan>> line_plans;
+  std::vector<std::unique_ptr<adp::CubePlan>> cube_plans;
 };
 
 namespace adp {
@@ -165,8 +184,8 @@ namespace adp {
 // Launch with programmatic stream serialization (PDL) when the context allows
 // it: the kernel must execute griddepcontrol.wait before reading anything the
 // previous kernel on the stream writes.
-template <class Kern, class Args>
-void launch_pdl(adp_ctx* ctx, Kern kern, dim3 grid, dim3 block, size_t smem, const Args& args) {
+template <class Kern, class... Args>
+void launch_pdl(adp_ctx* ctx, Kern kern, dim3 grid, dim3 block, size_t smem, const Args&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -177,7 +196,7 @@ void launch_pdl(adp_ctx* ctx, Kern kern, dim3 grid, dim3 block, size_t smem, con
   attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  ADP_CUDA(cudaLaunchKernelEx(&cfg, kern, args));
+  ADP_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
 }
 
 // ---- kernels (cheb_step.cu) ---------------------------------------------------
@@ -262,6 +281,9 @@ PairPlan* get_pair_plan(adp_csr* a, int64_t chunk_rows, int64_t gs, int64_t n_pa
 // blocks of rows with shifted column patterns. Returns false if not applicable.
 bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 const LinePlan* get_line_plan(adp_csr* a, int rows_per_block, int max_run);
+// The cube kernel (cheb_cube.cu): reuse across 2-D/3-D row blocks (tuning variants 111-118).
+bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+const CubePlan* get_cube_plan(adp_csr* a, int rows_per_line, int ly, int lz, int max_run);
 // Host copies of a device-created operator's arrays, downloaded on first use by the
 // host-side preprocessing (line plans, tilings, segments, the dense fallback).
 void ensure_host_copy(adp_csr* a);

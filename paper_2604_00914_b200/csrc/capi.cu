@@ -284,7 +284,7 @@ adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
     if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) ||
         (variant > 24 && variant < 31) || (variant > 33 && variant < 40) || (variant > 49 && variant < 51) ||
         (variant > 56 && variant < 61) || (variant > 66 && variant < 71) || (variant > 76 && variant < 81) ||
-        (variant > 98 && variant < 101) || variant > 108)
+        (variant > 98 && variant < 101) || (variant > 108 && variant < 111) || variant > 118)
       fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
     ctx->pair_variant = (variant > 70 && variant < 77) ? variant - 70 : 0;

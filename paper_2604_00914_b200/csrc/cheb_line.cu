@@ -774,6 +774,11 @@ bool dispatch_line(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
 
 }  // namespace
 
+CUtensorMap make_tensor_map_f64(const void* base, int64_t rows, int64_t width, int64_t ld_b, int box_rows,
+                                int box_words) {
+  return make_map(base, rows, width, ld_b, box_rows, box_words);
+}
+
 // Automatic choice (variant 0): the line kernel where it measured faster than
 // the lean kernel (tools/tune_step.py, profiles/r01_kernel_evolution.md): long
 // stencil rows (config 4: 27 entries, gather-latency bound) whose row blocks are

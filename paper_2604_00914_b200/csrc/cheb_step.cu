@@ -416,6 +416,7 @@ void launch_step_impl(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   // (cheb_row.cu) and this file's one-row-per-group kernel as tuning variants
   // and for 1-3 vectors.
   if (ctx->tile_ch > 0 && launch_step_tiled(ctx, mode, s)) return;
+  if (ctx->variant >= 111 && launch_step_cube(ctx, mode, s)) return;
   if ((ctx->variant == 0 || ctx->variant >= 81) && launch_step_line(ctx, mode, s)) return;
   if ((ctx->variant == 0 || ctx->variant >= 21) && launch_step_lean(ctx, mode, s)) return;
   if (ctx->variant > 10 && launch_step_row(ctx, mode, s)) return;

@@ -287,7 +287,7 @@ def test_config2_full_size_bitwise_low_degree(ctx, orc):
 # arithmetic. Stencil operators exercise the shifted-pattern blocks (and their
 # irregular faces), a random matrix the row-by-row fallbacks.
 VARIANTS = [0, 1, 11, 21, 22, 31, 33, 41, 42, 51, 56, 61, 62, 64, 71, 72, 73, 81, 82, 83, 84, 86, 88, 91, 92, 94, 97,
-            101, 102, 103, 104, 105, 106, 107, 108, 40]
+            101, 102, 103, 104, 105, 106, 107, 108, 40, 111, 112, 113, 114, 115, 116, 117, 118]
 
 
 @pytest.mark.parametrize("kind", ["lap7", "lap27", "random", "hermitian"])
