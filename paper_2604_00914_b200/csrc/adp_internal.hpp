@@ -72,6 +72,7 @@ struct adp_ctx {
   adp::DevBuf sched;      // task tickets of persistent kernels (self re-arming)
   bool pdl = true;        // programmatic dependent launch between degree steps (ADP_NO_PDL=1: off)
   bool auto_line = true;  // automatic line-kernel choice (ADP_NO_LINE=1: off, for A/B timing)
+  bool auto_cube = true;  // automatic cube-kernel choice for its full panels (ADP_NO_CUBE=1: off)
   bool sched_ready = false;
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;
@@ -283,6 +284,7 @@ bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 const LinePlan* get_line_plan(adp_csr* a, int rows_per_block, int max_run);
 // The cube kernel (cheb_cube.cu): reuse across 2-D/3-D row blocks (tuning variants 111-118).
 bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& args, int64_t vectors);
 const CubePlan* get_cube_plan(adp_csr* a, int rows_per_line, int ly, int lz, int max_run);
 // Host copies of a device-created operator's arrays, downloaded on first use by the
 // host-side preprocessing (line plans, tilings, segments, the dense fallback).

@@ -234,6 +234,8 @@ adp_status adp_ctx_create(int32_t device, adp_ctx** out) {
     ctx->pdl = !(no_pdl && no_pdl[0] == '1');
     const char* no_line = std::getenv("ADP_NO_LINE");
     ctx->auto_line = !(no_line && no_line[0] == '1');
+    const char* no_cube = std::getenv("ADP_NO_CUBE");
+    ctx->auto_cube = !(no_cube && no_cube[0] == '1');
     *out = ctx;
   });
 }

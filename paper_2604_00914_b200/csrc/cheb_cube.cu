@@ -374,7 +374,8 @@ template <class F>
 __host__ __device__ constexpr uint32_t cube_value_slot() {
   return static_cast<uint32_t>(kCubeValueSlot) * (sizeof(typename F::Val) / 8);
 }
-// rows per ring stage: one item's R + MM - 1 gathered rows, or a line's V and Y rows
+// rows per ring stage: one item's R + MM - 1 gathered rows, or (Step) a line's V and Y rows. (The own W
+// rows through the ring too -- 3R rows per stage -- measured slower: the larger stages cost occupancy.)
 template <int R, int MM, int MODE>
 __host__ __device__ constexpr int cube_stage_rows() {
   return MODE == static_cast<int>(StepMode::Step) && 2 * R > R + MM - 1 ? 2 * R : R + MM - 1;
@@ -733,8 +734,8 @@ bool dispatch_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
     case 112: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 2, 0.0);
     case 113: return launch_cube_cfg<F, 2, 2, 1, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
     case 114: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 115: return launch_cube_cfg<F, 4, 2, 1, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 116: return launch_cube_cfg<F, 2, 4, 1, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
+    case 115: return launch_cube_cfg<F, 1, 2, 2, 2, 3, 4, RP, 2>(ctx, mode, s, qv, 1, 0.0);
+    case 116: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 2, 0.0);
     case 117: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
     case 118: return launch_cube_cfg<F, 1, 2, 2, 2, 3, 3, RP, 3>(ctx, mode, s, qv, 2, 0.0);
     default: return false;
@@ -742,6 +743,15 @@ bool dispatch_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
 }
 
 }  // namespace
+
+// Automatic choice for the full 64-vector panels of a long-row real stencil operator (config 4):
+// 2 x 2 lines of 2 rows, 1 KB panels, 2 ring stages (tools/tune_step.py).
+bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
+  const adp_csr* a = s.a;
+  if (!ctx->auto_cube || a->dtype != ADP_F64 || s.row_begin != 0 || s.row_end != a->n_rows) return false;
+  return a->rp64 ? launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int64_t, 2>(ctx, mode, s, qv, 1, 0.5)
+                 : launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int32_t, 2>(ctx, mode, s, qv, 1, 0.5);
+}
 
 bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;

@@ -791,10 +791,11 @@ bool auto_line(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
   const bool long_rows = a->nnz >= 12 * a->n_rows;
   if (!long_rows || a->dtype != ADP_F64 || ctx->panel_cols != 0) return false;
   const int64_t full = qv / 64 * 64, rem = qv - full;
-  if (full > 0) {
+  if (full > 0) {  // full panels: the cube kernel where the operator has 3-D shifted blocks, else the line kernel
     StepArgs t = s;
     t.q = full * 2;
-    if (!launch_line_cfg<F, 2, 2, 3, RP, 3>(ctx, mode, t, full, 0.5)) return false;
+    if (!launch_cube_auto(ctx, mode, t, full) && !launch_line_cfg<F, 2, 2, 3, RP, 3>(ctx, mode, t, full, 0.5))
+      return false;
   } else if (get_line_plan(const_cast<adp_csr*>(a), 2, 3)->regular_frac < 0.5) {
     return false;
   }
