@@ -79,8 +79,10 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
  * kernel, 21-24 row-block union, 31-33 deeper gather batches, 41-46 column
  * segments, 51-56 lane-parallel metadata, 61-66 shared-memory row window,
  * 71-76 two degree steps per launch, 81-91 and 98 line kernel (register reuse across
- * shifted-pattern row blocks), 92-97 line kernel with a TMA ring. Other values
- * fail with ADP_ERR_CONFIG. */
+ * shifted-pattern row blocks), 92-97 line kernel with a TMA ring, 101-108 lean
+ * kernel walking several rows per warp, 111-118 cube kernel (runs shared by 2-D/3-D
+ * blocks of grid lines, TMA ring). Other values fail with
+ * ADP_ERR_CONFIG. */
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant);
 /* Tile-kernel knobs (0 = default): 16-byte vectors per lane per panel (1-4),
  * shared-memory pipeline stages, KiB per stage, resident CTAs per SM. */
