@@ -132,11 +132,16 @@ namespace adp {
 // Shifted-pattern row blocks of an operator for the line kernel (cheb_line.cu).
 struct LinePlan {
   int R = 0, mm = 0;
-  int64_t n_blocks = 0, n_regular = 0, n_patterns = 0, n_runs = 0;
+  bool band = false;          // band blocks allowed (register line kernel only)
+  int64_t n_blocks = 0, n_regular = 0, n_patterns = 0, n_runs = 0, n_band = 0;
   double regular_frac = 0.0;
   void* d_blk_pat = nullptr;  // int32[n_blocks]: pattern id, -1 = row by row
   void* d_pat_ptr = nullptr;  // int32[n_patterns+1]: runs of each pattern
-  void* d_runs = nullptr;     // int4[n_runs]: {first column - r0, entry index, length, 0}
+  void* d_runs = nullptr;     // int4[n_runs]: {first column - r0, entry index in the core, length, 0}
+  // Band blocks: only a core of consecutive columns is shared (shifted by one per row); each row's
+  // entries before it (prefix) and after it (suffix) run row by row. nullptr when no band block exists.
+  void* d_prefix = nullptr;   // int32[n_rows]: entries before the core (0 outside band blocks)
+  void* d_pat_len = nullptr;  // int32[n_patterns]: entries of each pattern's core
   ~LinePlan();
 };
 // Blocks of L = ly * lz lines of R consecutive rows (line l at r0 + off[l]) for the
@@ -281,7 +286,7 @@ PairPlan* get_pair_plan(adp_csr* a, int64_t chunk_rows, int64_t gs, int64_t n_pa
 // The line kernel (cheb_line.cu): register reuse of gathered rows across
 // blocks of rows with shifted column patterns. Returns false if not applicable.
 bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& args);
-const LinePlan* get_line_plan(adp_csr* a, int rows_per_block, int max_run);
+const LinePlan* get_line_plan(adp_csr* a, int rows_per_block, int max_run, bool band = false);
 // The cube kernel (cheb_cube.cu): reuse across 2-D/3-D row blocks (tuning variants 111-118).
 bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& args, int64_t vectors);
@@ -289,6 +294,10 @@ const CubePlan* get_cube_plan(adp_csr* a, int rows_per_line, int ly, int lz, int
 // Host copies of a device-created operator's arrays, downloaded on first use by the
 // host-side preprocessing (line plans, tilings, segments, the dense fallback).
 void ensure_host_copy(adp_csr* a);
+// A host-built plan's arrays have been copied with cudaMemcpy from pageable memory, which may return
+// before the DMA lands; kernels on the context's non-blocking stream are not ordered after it, so
+// every plan builder waits for its uploads (on the legacy stream that carried them) before use.
+inline void plan_uploads_done() { ADP_CUDA(cudaStreamSynchronize(cudaStreamLegacy)); }
 // Device-side CSR validation (CsrMatrix::validate, csr_matrix.hpp:101-116): returns 0 if
 // row_ptr is non-decreasing from 0 to nnz and every row's columns are strictly increasing in [0, n_cols).
 int validate_csr_device(adp_ctx* ctx, const int64_t* row_ptr, const int32_t* col, int64_t n_rows, int64_t n_cols,

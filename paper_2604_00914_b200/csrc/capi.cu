@@ -356,6 +356,7 @@ adp_status adp_csr_create(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, const in
         ADP_CUDA(cudaMemcpy(a->col_idx, col32.data(), nnz * 4, cudaMemcpyHostToDevice));
         ADP_CUDA(cudaMemcpy(a->values, values, nnz * eb, cudaMemcpyHostToDevice));
       }
+      adp::plan_uploads_done();  // pageable copies may return before their DMA lands (adp_internal.hpp)
       a->h_row_ptr.assign(row_ptr, row_ptr + n_rows + 1);
       a->h_col = std::move(col32);
       a->h_values = std::malloc(std::max<size_t>(nnz, 1) * eb);

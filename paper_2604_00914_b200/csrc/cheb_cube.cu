@@ -260,6 +260,7 @@ const CubePlan* get_cube_plan(adp_csr* a, int R, int ly, int lz, int mm) {
   up(&p->d_pat_nv, pat_nv.data(), pat_nv.size() * 4);
   up(&p->d_vals, vals.data(), vals.size());
   p->valid = true;
+  plan_uploads_done();
   a->cube_plans.push_back(std::move(p));
   return a->cube_plans.back().get();
 }

@@ -36,14 +36,35 @@ LinePlan::~LinePlan() {
   cudaFree(d_blk_pat);
   cudaFree(d_pat_ptr);
   cudaFree(d_runs);
+  cudaFree(d_prefix);
+  cudaFree(d_pat_len);
 }
 
-const LinePlan* get_line_plan(adp_csr* a, int R, int mm) {
+namespace {
+constexpr int64_t kMinCore = 32;  // shortest shared core worth a band block
+// Longest run of consecutive columns of a row: {entry index, length}.
+std::pair<int64_t, int64_t> longest_run(const int32_t* c, int64_t cnt) {
+  int64_t best = 0, bl = 0, k = 0;
+  while (k < cnt) {
+    int64_t m = 1;
+    while (k + m < cnt && c[k + m] == c[k + m - 1] + 1) ++m;
+    if (m > bl) {
+      bl = m;
+      best = k;
+    }
+    k += m;
+  }
+  return {best, bl};
+}
+}  // namespace
+
+const LinePlan* get_line_plan(adp_csr* a, int R, int mm, bool band) {
   for (auto& p : a->line_plans)
-    if (p->R == R && p->mm == mm) return p.get();
+    if (p->R == R && p->mm == mm && p->band == band) return p.get();
   auto p = std::make_unique<LinePlan>();
   p->R = R;
   p->mm = mm;
+  p->band = band;
   const int64_t n = a->n_rows;
   const int64_t nb = (n + R - 1) / R;
   ensure_host_copy(a);
@@ -55,6 +76,9 @@ const LinePlan* get_line_plan(adp_csr* a, int R, int mm) {
   std::vector<int32_t> runs;  // {relc, k, m, 0} per run
   std::vector<int32_t> sig;
   int64_t regular = 0;
+  std::vector<int32_t> prefix;  // band blocks: entries before the core, per row
+  std::vector<int32_t> pat_len;
+  int64_t n_band = 0;
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t r0 = b * R;
     if (r0 + R > n) break;
@@ -74,13 +98,34 @@ const LinePlan* get_line_plan(adp_csr* a, int R, int mm) {
           break;
         }
     }
+    // band block: every row's longest consecutive run is row r0's shifted by i (the rest row by row)
+    int64_t core_k0 = 0, core_len = cnt;
+    std::vector<int32_t> pre(static_cast<size_t>(R), 0);
+    bool is_band = false;
+    if (!ok && band) {
+      const auto [k0, len] = longest_run(&ci[rp[r0]], cnt);
+      bool bok = len >= kMinCore;
+      const int64_t c_start = bok ? static_cast<int64_t>(ci[rp[r0] + k0]) : 0;
+      for (int i = 0; i < R && bok; ++i) {
+        const int64_t ri = r0 + i, cnt_i = rp[ri + 1] - rp[ri];
+        const auto [ki, li] = longest_run(&ci[rp[ri]], cnt_i);
+        if (li != len || static_cast<int64_t>(ci[rp[ri] + ki]) != c_start + i || ki >= (int64_t{1} << 30)) bok = false;
+        else pre[i] = static_cast<int32_t>(ki);
+      }
+      if (bok) {
+        ok = true;
+        is_band = true;
+        core_k0 = k0;
+        core_len = len;
+      }
+    }
     if (!ok) continue;
     sig.clear();
-    const int32_t* c0 = &ci[rp[r0]];
+    const int32_t* c0 = &ci[rp[r0] + core_k0];
     int64_t k = 0;
-    while (k < cnt) {
+    while (k < core_len) {
       int64_t m = 1;
-      while (k + m < cnt && m < mm && c0[k + m] == c0[k + m - 1] + 1) ++m;
+      while (k + m < core_len && m < mm && c0[k + m] == c0[k + m - 1] + 1) ++m;
       sig.push_back(static_cast<int32_t>(static_cast<int64_t>(c0[k]) - r0));
       sig.push_back(static_cast<int32_t>(k));
       sig.push_back(static_cast<int32_t>(m));
@@ -95,8 +140,14 @@ const LinePlan* get_line_plan(adp_csr* a, int R, int mm) {
       ids.emplace(sig, id);
       runs.insert(runs.end(), sig.begin(), sig.end());
       pat_ptr.push_back(static_cast<int32_t>(runs.size() / 4));
+      pat_len.push_back(static_cast<int32_t>(core_len));
     } else {
       id = it->second;
+    }
+    if (is_band) {
+      if (prefix.empty()) prefix.assign(static_cast<size_t>(n), 0);
+      for (int i = 0; i < R; ++i) prefix[r0 + i] = pre[i];
+      ++n_band;
     }
     blk_pat[b] = id;
     ++regular;
@@ -114,6 +165,12 @@ const LinePlan* get_line_plan(adp_csr* a, int R, int mm) {
   up(&p->d_blk_pat, blk_pat.data(), blk_pat.size() * 4);
   up(&p->d_pat_ptr, pat_ptr.data(), pat_ptr.size() * 4);
   up(&p->d_runs, runs.data(), runs.size() * 4);
+  p->n_band = n_band;
+  if (n_band > 0) {
+    up(&p->d_prefix, prefix.data(), prefix.size() * 4);
+    up(&p->d_pat_len, pat_len.data(), pat_len.size() * 4);
+  }
+  plan_uploads_done();
   a->line_plans.push_back(std::move(p));
   return a->line_plans.back().get();
 }
@@ -138,6 +195,8 @@ struct LnArgs {
   const int32_t* blk_pat;
   const int32_t* pat_ptr;
   const int4* runs;
+  const int32_t* prefix;   // band plans: entries before each row's core (nullptr: no band block)
+  const int32_t* pat_len;  // band plans: core entries of each pattern
   uint32_t* sched;  // pipelined kernel: [0] next task ticket, [1] finished warps (both 0 between launches)
   double s0, s1, s2, s3;
 };
@@ -292,10 +351,32 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
       else
         acc[i][c] = make_double2(0.0, 0.0);
     }
-  if (pid >= 0) {  // shifted-pattern block: R full rows
+  // entries [e0, e1) of block row i, one by one (CSR order)
+  auto row_entries = [&](int i, int64_t e0, int64_t e1) {
+    for (int64_t e = e0; e < e1; ++e) {
+      const int cidx = __ldg(p.col + e);
+      const Val v = F::load(p.val, e);
+      const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        double2 wv = ok[c] ? __ldg(src + 32 * c) : make_double2(0.0, 0.0);
+        if constexpr (kFirst) wv = scale2(p.s2, wv);
+        acc[i][c] = F::mac(acc[i][c], v, wv);
+      }
+    }
+  };
+  if (pid >= 0) {  // shifted-pattern block: R full rows, or R rows sharing a shifted core (band plans)
     int64_t rs[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) rs[i] = ld_rp<RP>(p.row_ptr, r0 + i);
+    if (p.prefix) {  // each row's entries before the core
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int32_t pre = __ldg(p.prefix + r0 + i);
+        row_entries(i, rs[i], rs[i] + pre);
+        rs[i] += pre;
+      }
+    }
     const int32_t q0 = __ldg(p.pat_ptr + pid), q1 = __ldg(p.pat_ptr + pid + 1);
 #pragma unroll UNR
     for (int32_t qr = q0; qr < q1; ++qr) {
@@ -325,6 +406,11 @@ __global__ void __launch_bounds__(kThreads, MINB) cheb_line_kernel(const LnArgs 
           }
         }
       }
+    }
+    if (p.prefix) {  // each row's entries after the core
+      const int32_t clen = __ldg(p.pat_len + pid);
+#pragma unroll
+      for (int i = 0; i < R; ++i) row_entries(i, rs[i] + clen, ld_rp<RP>(p.row_ptr, r0 + i + 1));
     }
   } else {  // row by row, CSR order
 #pragma unroll
@@ -388,7 +474,7 @@ template <class F, int CH, int R, int MM, class RP, int MINB, int UNR = 1, bool 
 bool launch_line_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv, double min_regular) {
   const adp_csr* a = s.a;
   if (MASK ? (qv > 32 * CH || qv <= 32 * (CH - 1)) : qv % (32 * CH) != 0) return false;
-  const LinePlan* plan = get_line_plan(const_cast<adp_csr*>(a), R, MM);
+  const LinePlan* plan = get_line_plan(const_cast<adp_csr*>(a), R, MM, true);
   if (plan->regular_frac < min_regular) return false;
   constexpr int kWarps = kThreads / 32;
   const int epv = a->dtype == ADP_C128 ? 1 : 2;
@@ -412,6 +498,8 @@ bool launch_line_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
   k.blk_pat = static_cast<const int32_t*>(plan->d_blk_pat);
   k.pat_ptr = static_cast<const int32_t*>(plan->d_pat_ptr);
   k.runs = static_cast<const int4*>(plan->d_runs);
+  k.prefix = static_cast<const int32_t*>(plan->d_prefix);
+  k.pat_len = static_cast<const int32_t*>(plan->d_pat_len);
   k.s0 = s.s0;
   k.s1 = s.s1;
   k.s2 = s.s2;

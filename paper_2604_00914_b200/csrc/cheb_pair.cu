@@ -392,6 +392,7 @@ PairPlan* get_pair_plan(adp_csr* a, int64_t chunk_rows, int64_t gs, int64_t n_pa
     ADP_CUDA(cudaMalloc(&p->d_ghi, std::max<size_t>(nch * 4, 16)));
     ADP_CUDA(cudaMemcpy(p->d_glo, glo.data(), nch * 4, cudaMemcpyHostToDevice));
     ADP_CUDA(cudaMemcpy(p->d_ghi, ghi.data(), nch * 4, cudaMemcpyHostToDevice));
+    plan_uploads_done();
     a->pair_plans.push_back(std::move(p));
     plan = a->pair_plans.back().get();
   }

@@ -97,6 +97,7 @@ const Segments* get_segments(adp_csr* a, int R) {
   up(&s->d_col, col.data(), col.size() * 4);
   up(&s->d_mask, msk.data(), msk.size() * 4);
   up(&s->d_val, val.data(), val.size());
+  plan_uploads_done();
   a->segments.push_back(std::move(s));
   return a->segments.back().get();
 }

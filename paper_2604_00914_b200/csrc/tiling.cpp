@@ -131,6 +131,7 @@ const Tiling* get_tiling(adp_csr* a, int64_t panel_bytes, int64_t stage_bytes) {
   up(&t->d_dcol, dcol.data(), dcol.size() * 4);
   up(&t->d_blob, blob.data(), blob.size());
   t->distinct = static_cast<int64_t>(dcol.size());
+  plan_uploads_done();
   a->tilings.push_back(std::move(t));
   return a->tilings.back().get();
 }

@@ -290,11 +290,13 @@ VARIANTS = [0, 1, 11, 21, 22, 31, 33, 41, 42, 51, 56, 61, 62, 64, 71, 72, 73, 81
             101, 102, 103, 104, 105, 106, 107, 108, 40, 111, 112, 113, 114, 115, 116, 117, 118]
 
 
-@pytest.mark.parametrize("kind", ["lap7", "lap27", "random", "hermitian"])
+@pytest.mark.parametrize("kind", ["lap7", "lap27", "random", "hermitian", "band"])
 def test_kernel_variants_bitwise(ctx, orc, kind):
     from paper_2604_00914_b200 import configs
 
-    if kind == "lap7":
+    if kind == "band":  # config 5's structure (band + random off-band entries): the line kernel's band blocks
+        a = configs.random_banded_hermitian(600, 40, 4, seed=2)
+    elif kind == "lap7":
         a = configs.laplacian7_potential(11, -2.0, 2.0, seed=3)
     elif kind == "lap27":
         a = configs.dft_like_27pt(9, n_centres=4, seed=1)
