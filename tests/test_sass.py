@@ -1,8 +1,8 @@
 """SASS-level checks of libadp_b200.so (CPU only: cuobjdump, no GPU).
 
 * every kernel is compiled for sm_100a;
-* the TMA tile kernel really issues bulk copies (UBLKCP) and the row kernels
-  LDGSTS (cp.async);
+* the TMA tile kernel really issues bulk copies (UBLKCP), the line-ring and cube
+  kernels tensor-map tiles (UTMALDG) and the row kernels LDGSTS (cp.async);
 * no global access uses an odd-numbered uniform descriptor register: ptxas
   12.9 produced such code for cache-hinted cp.async in one kernel shape, and
   it faults at run time (illegal instruction) -- this guards the workaround;
@@ -59,6 +59,9 @@ def test_tma_and_async_copies_present(sass):
     assert linep and all(any("UTMALDG" in ln for ln in funcs[f]) for f in linep)
     pair = [f for f in funcs if "cheb_pair_kernel" in f]
     assert pair and all(any("UBLKCP" in ln for ln in funcs[f]) for f in pair)
+    # the cube kernel: gathered items (and V / Y rows) as 2-D tensor-map tiles, the block's values as a bulk copy
+    cube = [f for f in funcs if "cheb_cube_kernel" in f]
+    assert cube and all(any("UTMALDG" in ln for ln in funcs[f]) and any("UBLKCP" in ln for ln in funcs[f]) for f in cube)
 
 
 def test_no_odd_uniform_descriptors(sass):
@@ -73,7 +76,8 @@ def test_step_kernels_have_no_fma(sass):
     _, funcs = sass
     step = [f for f in funcs if re.search(r"cheb_\w+_kernel", f)]
     # every fused-step design: lean, lean2, union, seg, win, pair, line, linep, row, tile, step
-    for name in ("cheb_lean_kernel", "cheb_pair_kernel", "cheb_line_kernel", "cheb_linep_kernel", "cheb_win_kernel"):
+    for name in ("cheb_lean_kernel", "cheb_pair_kernel", "cheb_line_kernel", "cheb_linep_kernel", "cheb_win_kernel",
+                 "cheb_cube_kernel"):
         assert any(name in f for f in step), name
     assert step
     real = [f for f in step if "Cplx" not in f]
