@@ -402,23 +402,29 @@ __device__ __forceinline__ void tma2d_hint(void* dst, const CUtensorMap* tm, int
       : "memory");
 }
 
-// One warp per task (block, group of panels). The task's stream of TMA tile
-// copies -- per panel, each item's R + m - 1 gathered rows, then (Step mode)
-// each line's V and Y rows -- runs through a per-warp ring of S shared-memory
-// stages, S entries ahead of the consumer and across panel boundaries, so the
-// gathers' and streams' latency is covered by copies in flight rather than by
-// registers. The block's values sit in shared memory for the whole task in the
-// order the items consume them. Remainder blocks (listed rows) read V / Y directly.
-template <class F, int CH, int R, int L, int MM, int S, int MODE, class RP, int MINB>
+// One warp (SP = 1) or a pair of warps (SP = 2) per task (block, group of panels). The
+// task's stream of TMA tile copies -- per panel, each item's R + m - 1 gathered rows, then
+// (Step mode) each line's V and Y rows -- runs through a ring of S shared-memory stages,
+// S entries ahead of the consumers and across panel boundaries, so the gathers' and
+// streams' latency is covered by copies in flight rather than by registers. The block's
+// values sit in shared memory for the whole task in the order the items consume them.
+// With SP = 2 both warps read every item from the shared ring and each accumulates half
+// of the block's lines (half the registers, half the shared memory per warp: more
+// resident warps); they meet at a pair barrier before a stage is refilled. Remainder
+// blocks (listed rows) read V / Y directly.
+template <class F, int CH, int R, int L, int MM, int S, int MODE, class RP, int MINB, int SP, bool LAZY>
 __global__ void __launch_bounds__(kThreads, MINB)
     cheb_cube_kernel(const CbArgs p, const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_v,
                      const __grid_constant__ CUtensorMap tm_y) {
+  static_assert(SP == 1 || SP == 2, "one warp or a warp pair per task");
+  static_assert(L % SP == 0, "lines split evenly over the warps of a task");
   constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
   constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
   constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
   constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
   constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
-  constexpr int kWarps = kThreads / 32;
+  constexpr int kTasks = kThreads / 32 / SP;  // tasks per CTA
+  constexpr int LW = L / SP;                  // lines per warp
   constexpr uint32_t kPB = 32 * CH * 16u;
   constexpr int32_t kPE = static_cast<int32_t>(kPB / 8);  // panel width in fp64 words
   constexpr int kW = R + MM - 1;
@@ -426,26 +432,36 @@ __global__ void __launch_bounds__(kThreads, MINB)
   constexpr int kCS = (R * MM + 1) / 2 * 2;  // values per (item, line) chunk: [i * MM + t]
   using Val = typename F::Val;
   constexpr uint32_t kVS = cube_value_slot<F>();
-  constexpr uint32_t kWB = cube_warp_smem<F, CH, R, MM, S, MODE>();
-  // [(S + 1) mbarriers per warp, 128 B aligned][warp: block values | S stages of kSR row panels]
-  constexpr uint32_t kBarB = ((kWarps * (S + 1) * 8) + 127) / 128 * 128;
+  constexpr uint32_t kWB = cube_warp_smem<F, CH, R, MM, S, MODE>();  // per task
+  // [(S + 1) mbarriers per task, 128 B aligned][task: block values | S stages of kSR row panels]
+  constexpr uint32_t kBarB = ((kTasks * (S + 1) * 8) + 127) / 128 * 128;
   extern __shared__ __align__(128) uint8_t smem[];
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int32_t task = static_cast<int32_t>(blockIdx.x) * kWarps + warp;
-  if (task >= p.nblk * p.n_groups) return;
+  const int slot = warp / SP, half = warp % SP;
+  const int32_t task = static_cast<int32_t>(blockIdx.x) * kTasks + slot;
+  if (task >= p.nblk * p.n_groups) return;  // both warps of a pair leave together
   const int32_t grp = task / p.nblk;
   const int32_t b = task - grp * p.nblk;
   const int4 bk = __ldg(p.blk + b);  // {r0 (or index into the remainder list), pattern id, value offset}
   const int32_t r0 = bk.x, pid = bk.y;
   const int32_t pan0 = grp * p.gp, pan1 = min(pan0 + p.gp, p.n_panels);
   const uint64_t pol = policy_evict_first();
-  uint64_t* bar_v = reinterpret_cast<uint64_t*>(smem) + (S + 1) * warp;
+  uint64_t* bar_v = reinterpret_cast<uint64_t*>(smem) + (S + 1) * slot;
   uint64_t* bar_r = bar_v + 1;  // one per ring stage
-  uint8_t* ws = smem + kBarB + warp * kWB;
+  uint8_t* ws = smem + kBarB + slot * kWB;
   const Val* sv = reinterpret_cast<const Val*>(ws);
   double2* ring = reinterpret_cast<double2*>(ws + kVS);
+  const bool producer = half == 0;
+  auto task_sync = [&]() {
+    if constexpr (SP == 1) {
+      __syncwarp();
+    } else {
+      asm volatile("bar.sync %0, %1;\n" ::"r"(1 + slot), "r"(32 * SP) : "memory");
+    }
+  };
 
+  // line lw of this warp is block line half * LW + lw; its row i -> r0 + off[l] + i (remainder: listed)
   auto row_of = [&](int l, int i, bool& ok) -> int32_t {
     if (pid == -2) {
       const int32_t idx = r0 + l * R + i;
@@ -456,31 +472,32 @@ __global__ void __launch_bounds__(kThreads, MINB)
     return r0 + p.off[l] + i;
   };
   int32_t q0 = 0, nit = 0;
-  if (lane == 0) {
+  if (producer && lane == 0) {
     for (int st = 0; st <= S; ++st) mbar_init(bar_v + st, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (pid >= 0) {
     q0 = __ldg(p.pat_ptr + pid);
     nit = __ldg(p.pat_ptr + pid + 1) - q0;
-    if (lane == 0) {  // the block's values, in consumption order, once per task
+    if (producer && lane == 0) {  // the block's values, in consumption order, once per task
       const uint32_t bytes = static_cast<uint32_t>(__ldg(p.pat_nv + pid)) * static_cast<uint32_t>(sizeof(Val));
       const int64_t vo = (static_cast<int64_t>(static_cast<uint32_t>(bk.w)) << 32) | static_cast<uint32_t>(bk.z);
       mbar_arrive_expect_tx(bar_v, bytes);
       bulk_g2s(ws, static_cast<const Val*>(p.vals) + vo, bytes, bar_v);
     }
   }
-  __syncwarp();
+  task_sync();  // barriers initialised before any warp of the task waits on them
   asm volatile("griddepcontrol.wait;\n" ::: "memory");  // see pdl_wait_and_release (cheb_lean.cu)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const bool vy = kStep && pid != -2;  // V / Y rows through the ring
   const int32_t per = nit + (vy ? L : 0);
   const int32_t nstream = per * (pan1 - pan0);
-  // producer state (warp-uniform): next stream entry (panel pk, entry e) and its stage
+  // producer state (warp-uniform): next stream entry (panel pk, entry e) and its stage.
+  // V / Y entries are interleaved over the warps: entry nit + e carries line (e % SP) * LW + e / SP.
   int32_t pe = 0, ppk = 0, pst = 0;
   const int32_t npan = nstream > 0 ? pan1 - pan0 : 0;
-  auto produce = [&]() {  // lane 0 issues the copies of the next stream entry
-    if (ppk >= npan) return;
+  auto produce = [&]() {  // the producer warp's lane 0 issues the copies of the next stream entry
+    if (!producer || ppk >= npan) return;
     if (lane == 0) {
       double2* dst = ring + pst * kSR * 32 * CH;
       const int32_t x = (pan0 + ppk) * kPE;
@@ -489,7 +506,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
         mbar_arrive_expect_tx(bar_r + pst, kW * kPB);
         tma2d(dst, &tm_w, x, r0 + h.x, bar_r + pst);
       } else {
-        const int32_t row0 = r0 + p.off[pe - nit];
+        const int32_t e = pe - nit;
+        const int32_t row0 = r0 + p.off[(e % SP) * LW + e / SP];
         mbar_arrive_expect_tx(bar_r + pst, 2 * R * kPB);
         tma2d_hint(dst, &tm_v, x, row0, bar_r + pst, pol);
         tma2d_hint(dst + R * 32 * CH, &tm_y, x, row0, bar_r + pst, pol);
@@ -504,11 +522,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
   for (int k = 0; k < S; ++k) produce();
   if (pid >= 0) mbar_wait(bar_v, 0);
-  int32_t cst = 0;      // consumer stage
-  uint32_t cph = 0;     // its phase parity
-  auto consumed = [&]() {
-    __syncwarp();
-    produce();  // refill the stage just read
+  int32_t cst = 0;   // consumer stage
+  uint32_t cph = 0;  // its phase parity
+  auto consumed = [&]() {  // every warp of the task has read the stage: refill it
+    task_sync();
+    produce();
     if (++cst == S) {
       cst = 0;
       cph ^= 1u;
@@ -518,44 +536,50 @@ __global__ void __launch_bounds__(kThreads, MINB)
   for (int32_t panel = pan0; panel < pan1; ++panel) {
     const uint32_t voff = static_cast<uint32_t>(panel) * kPB + lane * 16u;
     const char* gb = p.g + voff;
-    double2 acc[L][R][CH];
+    double2 acc[LW][R][CH];
 #pragma unroll
-    for (int l = 0; l < L; ++l)
+    for (int lw = 0; lw < LW; ++lw)
 #pragma unroll
       for (int i = 0; i < R; ++i)
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
           if constexpr (kSpmmAcc) {
             bool ok;
-            const int32_t r = row_of(l, i, ok);
-            acc[l][i][c] = ok ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c)
-                              : make_double2(0.0, 0.0);
+            const int32_t r = row_of(half * LW + lw, i, ok);
+            acc[lw][i][c] = ok ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c)
+                               : make_double2(0.0, 0.0);
           } else {
-            acc[l][i][c] = make_double2(0.0, 0.0);
+            acc[lw][i][c] = make_double2(0.0, 0.0);
           }
         }
     if (pid >= 0) {  // shifted-pattern block: the union of the lines' runs, ascending
-      int32_t vo = 0;  // running chunk offset into the block's values
+      int32_t vo = 0;  // chunk offset of the item's first active line in the block's values
       for (int32_t qi = 0; qi < nit; ++qi) {
         const int4 h = __ldg(p.items + q0 + qi);  // {start - r0, length, line mask, -}
         const int m = h.y;
+        const uint32_t mask = static_cast<uint32_t>(h.z);
         mbar_wait(bar_r + cst, cph);
-        double2 w[kW][CH];
         const double2* sr = ring + cst * kSR * 32 * CH + lane;
+        double2 w[LAZY ? 1 : kW][CH];
+        if constexpr (!LAZY) {  // the item's rows into registers, the stage released at once
 #pragma unroll
-        for (int j = 0; j < kW; ++j)
+          for (int j = 0; j < kW; ++j)
 #pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            w[j][c] = sr[(j * CH + c) * 32];
-            if constexpr (kFirst) w[j][c] = scale2(p.s2, w[j][c]);  // W = c_d * Y on the fly
-          }
-        consumed();
+            for (int c = 0; c < CH; ++c) {
+              w[j][c] = sr[(j * CH + c) * 32];
+              if constexpr (kFirst) w[j][c] = scale2(p.s2, w[j][c]);  // W = c_d * Y on the fly
+            }
+          consumed();
+        }
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
-          if (h.z & (1 << l)) {
+        for (int lw = 0; lw < LW; ++lw) {
+          const int l = half * LW + lw;
+          if (mask & (1u << l)) {
+            // chunks are stored per item in ascending line order
+            const int32_t co = vo + kCS * __popc(mask & ((1u << l) - 1u));
             Val v[kCS];
             if constexpr (sizeof(Val) == 8) {
-              const double2* cv = reinterpret_cast<const double2*>(sv + vo);
+              const double2* cv = reinterpret_cast<const double2*>(sv + co);
 #pragma unroll
               for (int e = 0; e < kCS / 2; ++e) {
                 const double2 t2 = cv[e];
@@ -564,16 +588,36 @@ __global__ void __launch_bounds__(kThreads, MINB)
               }
             } else {
 #pragma unroll
-              for (int e = 0; e < kCS; ++e) v[e] = sv[vo + e];
+              for (int e = 0; e < kCS; ++e) v[e] = sv[co + e];
             }
-            vo += kCS;
-            if (m == MM) {
+            if constexpr (LAZY) {
+              // one gathered row at a time, read from the stage: row j feeds (i, t = j - i); for a
+              // fixed row i, t ascends with j, so each row still accumulates in column order
+#pragma unroll
+              for (int j = 0; j < kW; ++j) {
+                if (j < R + m - 1) {
+#pragma unroll
+                  for (int c = 0; c < CH; ++c) {
+                    w[0][c] = sr[(j * CH + c) * 32];
+                    if constexpr (kFirst) w[0][c] = scale2(p.s2, w[0][c]);
+                  }
+#pragma unroll
+                  for (int i = 0; i < R; ++i) {
+                    const int t = j - i;
+                    if (t >= 0 && t < MM && t < m) {
+#pragma unroll
+                      for (int c = 0; c < CH; ++c) acc[lw][i][c] = F::mac(acc[lw][i][c], v[i * MM + t], w[0][c]);
+                    }
+                  }
+                }
+              }
+            } else if (m == MM) {
 #pragma unroll
               for (int i = 0; i < R; ++i)
 #pragma unroll
                 for (int t = 0; t < MM; ++t)
 #pragma unroll
-                  for (int c = 0; c < CH; ++c) acc[l][i][c] = F::mac(acc[l][i][c], v[i * MM + t], w[i + t][c]);
+                  for (int c = 0; c < CH; ++c) acc[lw][i][c] = F::mac(acc[lw][i][c], v[i * MM + t], w[i + t][c]);
             } else {
 #pragma unroll
               for (int i = 0; i < R; ++i)
@@ -581,19 +625,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 for (int t = 0; t < MM; ++t)
                   if (t < m) {
 #pragma unroll
-                    for (int c = 0; c < CH; ++c) acc[l][i][c] = F::mac(acc[l][i][c], v[i * MM + t], w[i + t][c]);
+                    for (int c = 0; c < CH; ++c) acc[lw][i][c] = F::mac(acc[lw][i][c], v[i * MM + t], w[i + t][c]);
                   }
             }
           }
         }
+        if constexpr (LAZY) consumed();  // every read of the stage done
+        vo += kCS * __popc(mask);
       }
     } else {  // row by row, CSR order
 #pragma unroll
-      for (int l = 0; l < L; ++l)
+      for (int lw = 0; lw < LW; ++lw)
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           bool ok;
-          const int32_t r = row_of(l, i, ok);
+          const int32_t r = row_of(half * LW + lw, i, ok);
           if (ok) {
             const RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r));
             const RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r + 1));
@@ -606,63 +652,70 @@ __global__ void __launch_bounds__(kThreads, MINB)
               for (int c = 0; c < CH; ++c) {
                 double2 wv = __ldg(src + 32 * c);
                 if constexpr (kFirst) wv = scale2(p.s2, wv);
-                acc[l][i][c] = F::mac(acc[l][i][c], v, wv);
+                acc[lw][i][c] = F::mac(acc[lw][i][c], v, wv);
               }
             }
           }
         }
     }
+    // epilogue: V / Y entries arrive interleaved over the warps (lw, then the warp that owns it)
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-      const double2* sr = ring + cst * kSR * 32 * CH + lane;  // this line's V / Y rows (Step, vy)
-      if constexpr (kStep) {
-        if (vy) mbar_wait(bar_r + cst, cph);
-      }
+    for (int lw = 0; lw < LW; ++lw) {
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        bool ok;
-        const int64_t r = row_of(l, i, ok);
-        if (!ok) continue;
-        const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
-        char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          double2 own = make_double2(0.0, 0.0);
-          if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
-          double2 res;
-          if constexpr (kStep) {
-            // v = (((s0 * aw) + (s1 * w)) - v) + (s2 * y)   (cheb_filter.cpp:170-171, 176-177)
-            double2 vv, yy;
-            if (vy) {
-              vv = sr[(i * CH + c) * 32];
-              yy = sr[((R + i) * CH + c) * 32];
-            } else {
-              vv = __ldg(reinterpret_cast<const double2*>(p.vin + static_cast<uint64_t>(r) * p.ldg_b + voff + 512 * c));
-              yy = __ldg(reinterpret_cast<const double2*>(p.yin + static_cast<uint64_t>(r) * p.ldy_b + voff + 512 * c));
-            }
-            res = add2(sub2(add2(scale2(p.s0, acc[l][i][c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
-          } else if constexpr (kFirst) {
-            // w = c_d * y ; v = (2 l1) * aw + (2 l2 + c_{d-1}/c_d) * w   (cheb_filter.cpp:162-165)
-            const double2 wn = scale2(p.s2, own);
-            st_hint(p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c, wn, pol);
-            res = add2(scale2(p.s0, acc[l][i][c]), scale2(p.s1, wn));
-          } else if constexpr (kDeg1) {
-            // c0 * x + c1 * (l1 * ax + l2 * x)   (cheb_filter.cpp:154)
-            res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[l][i][c]), scale2(p.s3, own))));
-          } else {
-            res = acc[l][i][c];
-          }
-          st_hint(ob + 512 * c, res, pol);
+      for (int hh = 0; hh < SP; ++hh) {
+        const double2* sr = ring + cst * kSR * 32 * CH + lane;  // line hh * LW + lw's V / Y rows (Step, vy)
+        if constexpr (kStep) {
+          if (vy) mbar_wait(bar_r + cst, cph);
         }
-      }
-      if constexpr (kStep) {
-        if (vy) consumed();
+        if (hh == half) {
+          const int l = half * LW + lw;
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            bool ok;
+            const int64_t r = row_of(l, i, ok);
+            if (!ok) continue;
+            const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
+            char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+              double2 own = make_double2(0.0, 0.0);
+              if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
+              double2 res;
+              if constexpr (kStep) {
+                // v = (((s0 * aw) + (s1 * w)) - v) + (s2 * y)   (cheb_filter.cpp:170-171, 176-177)
+                double2 vv, yy;
+                if (vy) {
+                  vv = sr[(i * CH + c) * 32];
+                  yy = sr[((R + i) * CH + c) * 32];
+                } else {
+                  vv = __ldg(reinterpret_cast<const double2*>(p.vin + static_cast<uint64_t>(r) * p.ldg_b + voff + 512 * c));
+                  yy = __ldg(reinterpret_cast<const double2*>(p.yin + static_cast<uint64_t>(r) * p.ldy_b + voff + 512 * c));
+                }
+                res = add2(sub2(add2(scale2(p.s0, acc[lw][i][c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
+              } else if constexpr (kFirst) {
+                // w = c_d * y ; v = (2 l1) * aw + (2 l2 + c_{d-1}/c_d) * w   (cheb_filter.cpp:162-165)
+                const double2 wn = scale2(p.s2, own);
+                st_hint(p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c, wn, pol);
+                res = add2(scale2(p.s0, acc[lw][i][c]), scale2(p.s1, wn));
+              } else if constexpr (kDeg1) {
+                // c0 * x + c1 * (l1 * ax + l2 * x)   (cheb_filter.cpp:154)
+                res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[lw][i][c]), scale2(p.s3, own))));
+              } else {
+                res = acc[lw][i][c];
+              }
+              st_hint(ob + 512 * c, res, pol);
+            }
+          }
+        }
+        if constexpr (kStep) {
+          if (vy) consumed();
+        }
       }
     }
   }
 }
 
-template <class F, int CH, int R, int LY, int LZ, int MM, int S, class RP, int MINB>
+template <class F, int CH, int R, int LY, int LZ, int MM, int S, class RP, int MINB, int SP = 1, bool LAZY = false>
 bool launch_cube_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv, int gp, double min_regular) {
   constexpr int L = LY * LZ;
   const adp_csr* a = s.a;
@@ -702,24 +755,25 @@ bool launch_cube_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
   k.s3 = s.s3;
   const int64_t total = plan->n_blocks * k.n_groups;
   if (total >= (int64_t{1} << 31)) return false;
-  const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
+  const int grid = static_cast<int>((total + kWarps / SP - 1) / (kWarps / SP));
   const int64_t width = qv * 2;  // fp64 words per row (vectors of 16 B)
   constexpr int kPE = 32 * CH * 2;
   const CUtensorMap tm_w = make_tensor_map_f64(s.gsrc, a->n_cols, width, k.ldg_b, R + MM - 1, kPE);
   const CUtensorMap tm_v = mode == StepMode::Step ? make_tensor_map_f64(s.vin, a->n_rows, width, k.ldg_b, R, kPE) : tm_w;
   const CUtensorMap tm_y = mode == StepMode::Step ? make_tensor_map_f64(s.yin, a->n_rows, width, k.ldy_b, R, kPE) : tm_w;
   auto run = [&](auto kern, uint32_t warp_bytes) {
-    const size_t smem = ((kWarps * (S + 1) * 8) + 127) / 128 * 128 + static_cast<size_t>(kWarps) * warp_bytes;
+    constexpr int kTasks = kWarps / SP;
+    const size_t smem = ((kTasks * (S + 1) * 8) + 127) / 128 * 128 + static_cast<size_t>(kTasks) * warp_bytes;
     if (smem > 48 * 1024)
       ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     launch_pdl(ctx, kern, dim3(grid), dim3(kThreads), smem, k, tm_w, tm_v, tm_y);
   };
   switch (mode) {
-    case StepMode::First: run(cheb_cube_kernel<F, CH, R, L, MM, S, 0, RP, MINB>, cube_warp_smem<F, CH, R, MM, S, 0>()); break;
-    case StepMode::Step: run(cheb_cube_kernel<F, CH, R, L, MM, S, 1, RP, MINB>, cube_warp_smem<F, CH, R, MM, S, 1>()); break;
-    case StepMode::Deg1: run(cheb_cube_kernel<F, CH, R, L, MM, S, 2, RP, MINB>, cube_warp_smem<F, CH, R, MM, S, 2>()); break;
-    case StepMode::Spmm: run(cheb_cube_kernel<F, CH, R, L, MM, S, 3, RP, MINB>, cube_warp_smem<F, CH, R, MM, S, 3>()); break;
-    case StepMode::SpmmAcc: run(cheb_cube_kernel<F, CH, R, L, MM, S, 4, RP, MINB>, cube_warp_smem<F, CH, R, MM, S, 4>()); break;
+    case StepMode::First: run(cheb_cube_kernel<F, CH, R, L, MM, S, 0, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 0>()); break;
+    case StepMode::Step: run(cheb_cube_kernel<F, CH, R, L, MM, S, 1, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 1>()); break;
+    case StepMode::Deg1: run(cheb_cube_kernel<F, CH, R, L, MM, S, 2, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 2>()); break;
+    case StepMode::Spmm: run(cheb_cube_kernel<F, CH, R, L, MM, S, 3, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 3>()); break;
+    case StepMode::SpmmAcc: run(cheb_cube_kernel<F, CH, R, L, MM, S, 4, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 4>()); break;
   }
   ADP_LAUNCH_CHECK();
   ctx->launches += 1;
@@ -735,10 +789,10 @@ bool dispatch_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
     case 112: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 2, 0.0);
     case 113: return launch_cube_cfg<F, 2, 2, 1, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
     case 114: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 115: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 1, RP, 3>(ctx, mode, s, qv, 1, 0.0);
-    case 116: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 1, RP, 2>(ctx, mode, s, qv, 1, 0.0);
+    case 115: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 3, RP, 3, 2, true>(ctx, mode, s, qv, 1, 0.0);
+    case 116: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 3, RP, 2, 1, true>(ctx, mode, s, qv, 1, 0.0);
     case 117: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 118: return launch_cube_cfg<F, 2, 1, 2, 2, 3, 3, RP, 2>(ctx, mode, s, qv, 1, 0.0);
+    case 118: return launch_cube_cfg<F, 2, 2, 4, 2, 3, 3, RP, 2, 2, true>(ctx, mode, s, qv, 1, 0.0);
     default: return false;
   }
 }
