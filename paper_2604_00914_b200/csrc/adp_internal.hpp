@@ -149,6 +149,7 @@ struct LinePlan {
 constexpr int64_t kCubeValueSlot = 2048;  // bytes of shared memory per warp for a block's fp64 values (x2 complex)
 struct CubePlan {
   int R = 0, ly = 0, lz = 0, mm = 0;
+  int64_t row_begin = 0, row_end = 0;  // the rows the blocks cover (a launch's row range)
   bool valid = false;         // strides found and blocks built
   int64_t sy = 0, sz = 0;     // line strides derived from the dominant pattern
   int32_t off[8] = {};
@@ -290,7 +291,8 @@ const LinePlan* get_line_plan(adp_csr* a, int rows_per_block, int max_run, bool 
 // The cube kernel (cheb_cube.cu): reuse across 2-D/3-D row blocks (tuning variants 111-118).
 bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& args, int64_t vectors);
-const CubePlan* get_cube_plan(adp_csr* a, int rows_per_line, int ly, int lz, int max_run);
+const CubePlan* get_cube_plan(adp_csr* a, int rows_per_line, int ly, int lz, int max_run, int64_t row_begin,
+                              int64_t row_end);
 // Host copies of a device-created operator's arrays, downloaded on first use by the
 // host-side preprocessing (line plans, tilings, segments, the dense fallback).
 void ensure_host_copy(adp_csr* a);

@@ -104,14 +104,19 @@ bool detect_strides(const adp_csr* a, int mm, int64_t& sy, int64_t& sz) {
 
 }  // namespace
 
-const CubePlan* get_cube_plan(adp_csr* a, int R, int ly, int lz, int mm) {
+// Blocks cover rows [rb, re) (a launch's row range: the whole operator, or a rank's interior rows in
+// the row-partitioned filter); rows of the range outside every full block are listed as remainder.
+const CubePlan* get_cube_plan(adp_csr* a, int R, int ly, int lz, int mm, int64_t rb, int64_t re) {
   for (auto& p : a->cube_plans)
-    if (p->R == R && p->ly == ly && p->lz == lz && p->mm == mm) return p.get();
+    if (p->R == R && p->ly == ly && p->lz == lz && p->mm == mm && p->row_begin == rb && p->row_end == re)
+      return p.get();
   auto p = std::make_unique<CubePlan>();
   p->R = R;
   p->ly = ly;
   p->lz = lz;
   p->mm = mm;
+  p->row_begin = rb;
+  p->row_end = re;
   const int L = ly * lz;
   ensure_host_copy(a);
   int64_t sy = 0, sz = 0;
@@ -127,7 +132,7 @@ const CubePlan* get_cube_plan(adp_csr* a, int R, int ly, int lz, int mm) {
     for (int j = 0; j < ly; ++j) p->off[k * ly + j] = static_cast<int32_t>(j * sy + k * sz);
   const std::vector<int64_t>& rp = a->h_row_ptr;
   const std::vector<int32_t>& ci = a->h_col;
-  std::vector<uint8_t> taken(static_cast<size_t>(n), 0);
+  std::vector<uint8_t> taken(static_cast<size_t>(re - rb), 0);  // indexed r - rb
   std::vector<int32_t> blk;  // {r0, pattern} pairs
   std::vector<int32_t> rem;
   std::map<std::vector<int32_t>, int32_t> ids;
@@ -143,21 +148,21 @@ const CubePlan* get_cube_plan(adp_csr* a, int R, int ly, int lz, int mm) {
   std::map<std::pair<int64_t, int64_t>, std::array<int32_t, 8>> union_items;
   std::vector<int32_t> sig;
   int64_t regular = 0;
-  for (int64_t r0 = 0; r0 < n; ++r0) {
-    if (taken[r0]) continue;
+  for (int64_t r0 = rb; r0 < re; ++r0) {
+    if (taken[r0 - rb]) continue;
     bool fits = true;
     for (int l = 0; l < L && fits; ++l)
       for (int i = 0; i < R && fits; ++i) {
         const int64_t r = r0 + p->off[l] + i;
-        if (r >= n || taken[r]) fits = false;
+        if (r >= re || taken[r - rb]) fits = false;
       }
     if (!fits) {
-      taken[r0] = 1;
+      taken[r0 - rb] = 1;
       rem.push_back(static_cast<int32_t>(r0));
       continue;
     }
     for (int l = 0; l < L; ++l)
-      for (int i = 0; i < R; ++i) taken[r0 + p->off[l] + i] = 1;
+      for (int i = 0; i < R; ++i) taken[r0 + p->off[l] + i - rb] = 1;
     int32_t pid = -1;
     const int64_t cnt = rp[r0 + 1] - rp[r0];
     bool ok = cnt > 0 && cnt < 32768;
@@ -247,7 +252,7 @@ const CubePlan* get_cube_plan(adp_csr* a, int R, int ly, int lz, int mm) {
   p->n_rem = static_cast<int64_t>(rem.size());
   p->n_patterns = static_cast<int64_t>(ids.size());
   p->n_items = static_cast<int64_t>(items.size() / 4);
-  p->regular_rows_frac = n > 0 ? static_cast<double>(regular * per) / static_cast<double>(n) : 0.0;
+  p->regular_rows_frac = re > rb ? static_cast<double>(regular * per) / static_cast<double>(re - rb) : 0.0;
   ADP_CUDA(cudaSetDevice(a->ctx->device));
   auto up = [&](void** dst, const void* src, size_t bytes) {
     ADP_CUDA(cudaMalloc(dst, std::max<size_t>(bytes, 16)));
@@ -720,7 +725,7 @@ bool launch_cube_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
   constexpr int L = LY * LZ;
   const adp_csr* a = s.a;
   if (qv % (32 * CH) != 0) return false;
-  const CubePlan* plan = get_cube_plan(const_cast<adp_csr*>(a), R, LY, LZ, MM);
+  const CubePlan* plan = get_cube_plan(const_cast<adp_csr*>(a), R, LY, LZ, MM, s.row_begin, s.row_end);
   if (!plan->valid || plan->regular_rows_frac < min_regular) return false;
   constexpr int kWarps = kThreads / 32;
   const int epv = a->dtype == ADP_C128 ? 1 : 2;
@@ -803,7 +808,7 @@ bool dispatch_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
 // 2 x 2 lines of 2 rows, 1 KB panels, 2 ring stages (tools/tune_step.py).
 bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
   const adp_csr* a = s.a;
-  if (!ctx->auto_cube || a->dtype != ADP_F64 || s.row_begin != 0 || s.row_end != a->n_rows) return false;
+  if (!ctx->auto_cube || a->dtype != ADP_F64) return false;
   return a->rp64 ? launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int64_t, 2>(ctx, mode, s, qv, 1, 0.5)
                  : launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int32_t, 2>(ctx, mode, s, qv, 1, 0.5);
 }
@@ -811,7 +816,7 @@ bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv
 bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
   if (ctx->variant < 111 || ctx->variant > 118) return false;
-  if (s.row_begin != 0 || s.row_end != a->n_rows || a->n_rows >= (int64_t{1} << 30)) return false;
+  if (a->n_rows >= (int64_t{1} << 30)) return false;
   const bool cplx = a->dtype == ADP_C128;
   const int epv = cplx ? 1 : 2;
   const int64_t qv = (s.q + epv - 1) / epv;

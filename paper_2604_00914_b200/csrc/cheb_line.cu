@@ -908,12 +908,18 @@ bool auto_line(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
 
 bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
-  if (s.row_begin != 0 || s.row_end != a->n_rows || a->n_rows >= (int64_t{1} << 30)) return false;
+  if (a->n_rows >= (int64_t{1} << 30)) return false;
   const bool cplx = a->dtype == ADP_C128;
   const int epv = cplx ? 1 : 2;
   const int64_t qv = (s.q + epv - 1) / epv;  // odd real widths: the padding column of the (even) ld rides along
   for (int64_t ld : {s.ld, s.ld_y, s.ld_out})
     if (ld % epv != 0 || (ld / epv) * 16 >= (int64_t{1} << 32)) return false;
+  if (s.row_begin != 0 || s.row_end != a->n_rows) {
+    // a row range (a rank's interior rows in the row-partitioned filter): the cube kernel plans its
+    // blocks inside the range; the line kernel and ragged tails need whole operators
+    return ctx->variant == 0 && !cplx && ctx->auto_line && a->nnz >= 12 * a->n_rows && ctx->panel_cols == 0 &&
+           qv % 64 == 0 && launch_cube_auto(ctx, mode, s, qv);
+  }
   if (ctx->variant == 0) {
     if (cplx || !ctx->auto_line) return false;
     return a->rp64 ? auto_line<RealN, int64_t>(ctx, mode, s, qv) : auto_line<RealN, int32_t>(ctx, mode, s, qv);

@@ -115,7 +115,8 @@ def test_emulated_ranks_bitwise(orc, world, degree, q):
 # waits on a concurrently running one. Bitwise equal to the single-device filter; two calls
 # back to back, ragged and narrow widths (narrow ones push with the copy kernel).
 @pytest.mark.parametrize("world,degree,q,kind", [(2, 12, 64, "lap"), (3, 7, 6, "lap"), (2, 1, 130, "lap"),
-                                                  (4, 20, 256, "lap"), (2, 9, 2, "lap"), (3, 5, 100, "27pt")])
+                                                  (4, 20, 256, "lap"), (2, 9, 2, "lap"), (3, 5, 100, "27pt"),
+                                                  (2, 6, 256, "27pt")])  # interior rows: cube kernel, ranged plan
 def test_peer_halo_lockstep_bitwise(orc, world, degree, q, kind):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -178,6 +179,13 @@ def _ipc_worker(rank, port, out_path):
     untouched = float(blk.abs().sum()) == float(blk[3 + 20 + peer:8 + 20 + peer].abs().sum())
     with open(f"{out_path}.{rank}", "w") as fh:
         fh.write(f"{int(ok_rows)} {int(untouched)} {int(counters[peer])}\n")
+    # teardown order: drop the peer's imported mappings, then wait until BOTH processes have done so
+    # before either exits (an exporter leaving while its peer still maps its memory can kill the peer)
+    del pblk, pcnt, d
+    import gc
+
+    gc.collect()
+    torch.cuda.synchronize()
     dist.barrier()
     dist.destroy_process_group()
 
