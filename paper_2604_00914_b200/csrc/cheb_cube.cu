@@ -616,11 +616,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
                   }
                 }
               }
-            } else if (m == MM) {
+            } else if (m == MM) {  // position-major: the R x CH accumulators' chains interleave
 #pragma unroll
-              for (int i = 0; i < R; ++i)
+              for (int t = 0; t < MM; ++t)
 #pragma unroll
-                for (int t = 0; t < MM; ++t)
+                for (int i = 0; i < R; ++i)
 #pragma unroll
                   for (int c = 0; c < CH; ++c) acc[lw][i][c] = F::mac(acc[lw][i][c], v[i * MM + t], w[i + t][c]);
             } else {
