@@ -272,7 +272,6 @@ const CubePlan* get_cube_plan(adp_csr* a, int R, int ly, int lz, int mm, int64_t
 
 namespace {
 
-constexpr int kThreads = 256;
 
 struct CbArgs {
   const void* row_ptr;
@@ -417,8 +416,8 @@ __device__ __forceinline__ void tma2d_hint(void* dst, const CUtensorMap* tm, int
 // of the block's lines (half the registers, half the shared memory per warp: more
 // resident warps); they meet at a pair barrier before a stage is refilled. Remainder
 // blocks (listed rows) read V / Y directly.
-template <class F, int CH, int R, int L, int MM, int S, int MODE, class RP, int MINB, int SP, bool LAZY>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <class F, int CH, int R, int L, int MM, int S, int MODE, class RP, int MINB, int SP, bool LAZY, int NT>
+__global__ void __launch_bounds__(NT, MINB)
     cheb_cube_kernel(const CbArgs p, const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_v,
                      const __grid_constant__ CUtensorMap tm_y) {
   static_assert(SP == 1 || SP == 2, "one warp or a warp pair per task");
@@ -428,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
   constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
   constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
-  constexpr int kTasks = kThreads / 32 / SP;  // tasks per CTA
+  constexpr int kTasks = NT / 32 / SP;  // tasks per CTA
   constexpr int LW = L / SP;                  // lines per warp
   constexpr uint32_t kPB = 32 * CH * 16u;
   constexpr int32_t kPE = static_cast<int32_t>(kPB / 8);  // panel width in fp64 words
@@ -720,14 +719,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
-template <class F, int CH, int R, int LY, int LZ, int MM, int S, class RP, int MINB, int SP = 1, bool LAZY = false>
+template <class F, int CH, int R, int LY, int LZ, int MM, int S, class RP, int MINB, int SP = 1, bool LAZY = false,
+          int NT = 256>
 bool launch_cube_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv, int gp, double min_regular) {
   constexpr int L = LY * LZ;
   const adp_csr* a = s.a;
   if (qv % (32 * CH) != 0) return false;
   const CubePlan* plan = get_cube_plan(const_cast<adp_csr*>(a), R, LY, LZ, MM, s.row_begin, s.row_end);
   if (!plan->valid || plan->regular_rows_frac < min_regular) return false;
-  constexpr int kWarps = kThreads / 32;
+  constexpr int kWarps = NT / 32;
   const int epv = a->dtype == ADP_C128 ? 1 : 2;
   CbArgs k{};
   k.row_ptr = a->row_ptr;
@@ -771,14 +771,14 @@ bool launch_cube_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
     const size_t smem = ((kTasks * (S + 1) * 8) + 127) / 128 * 128 + static_cast<size_t>(kTasks) * warp_bytes;
     if (smem > 48 * 1024)
       ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    launch_pdl(ctx, kern, dim3(grid), dim3(kThreads), smem, k, tm_w, tm_v, tm_y);
+    launch_pdl(ctx, kern, dim3(grid), dim3(NT), smem, k, tm_w, tm_v, tm_y);
   };
   switch (mode) {
-    case StepMode::First: run(cheb_cube_kernel<F, CH, R, L, MM, S, 0, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 0>()); break;
-    case StepMode::Step: run(cheb_cube_kernel<F, CH, R, L, MM, S, 1, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 1>()); break;
-    case StepMode::Deg1: run(cheb_cube_kernel<F, CH, R, L, MM, S, 2, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 2>()); break;
-    case StepMode::Spmm: run(cheb_cube_kernel<F, CH, R, L, MM, S, 3, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 3>()); break;
-    case StepMode::SpmmAcc: run(cheb_cube_kernel<F, CH, R, L, MM, S, 4, RP, MINB, SP, LAZY>, cube_warp_smem<F, CH, R, MM, S, 4>()); break;
+    case StepMode::First: run(cheb_cube_kernel<F, CH, R, L, MM, S, 0, RP, MINB, SP, LAZY, NT>, cube_warp_smem<F, CH, R, MM, S, 0>()); break;
+    case StepMode::Step: run(cheb_cube_kernel<F, CH, R, L, MM, S, 1, RP, MINB, SP, LAZY, NT>, cube_warp_smem<F, CH, R, MM, S, 1>()); break;
+    case StepMode::Deg1: run(cheb_cube_kernel<F, CH, R, L, MM, S, 2, RP, MINB, SP, LAZY, NT>, cube_warp_smem<F, CH, R, MM, S, 2>()); break;
+    case StepMode::Spmm: run(cheb_cube_kernel<F, CH, R, L, MM, S, 3, RP, MINB, SP, LAZY, NT>, cube_warp_smem<F, CH, R, MM, S, 3>()); break;
+    case StepMode::SpmmAcc: run(cheb_cube_kernel<F, CH, R, L, MM, S, 4, RP, MINB, SP, LAZY, NT>, cube_warp_smem<F, CH, R, MM, S, 4>()); break;
   }
   ADP_LAUNCH_CHECK();
   ctx->launches += 1;
@@ -797,7 +797,7 @@ bool dispatch_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
     case 115: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 3, RP, 3, 2, true>(ctx, mode, s, qv, 1, 0.0);
     case 116: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 3, RP, 2, 1, true>(ctx, mode, s, qv, 1, 0.0);
     case 117: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 118: return launch_cube_cfg<F, 2, 2, 4, 2, 3, 3, RP, 2, 2, true>(ctx, mode, s, qv, 1, 0.0);
+    case 118: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.0);
     default: return false;
   }
 }
@@ -805,12 +805,12 @@ bool dispatch_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
 }  // namespace
 
 // Automatic choice for the full 64-vector panels of a long-row real stencil operator (config 4):
-// 2 x 2 lines of 2 rows, 1 KB panels, 2 ring stages (tools/tune_step.py).
+// 2 x 2 lines of 2 rows, 1 KB panels, 2 ring stages, 4-warp CTAs (tools/tune_step.py).
 bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
   const adp_csr* a = s.a;
   if (!ctx->auto_cube || a->dtype != ADP_F64) return false;
-  return a->rp64 ? launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int64_t, 2>(ctx, mode, s, qv, 1, 0.5)
-                 : launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int32_t, 2>(ctx, mode, s, qv, 1, 0.5);
+  return a->rp64 ? launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int64_t, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.5)
+                 : launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int32_t, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.5);
 }
 
 bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
