@@ -794,8 +794,8 @@ bool dispatch_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
     case 112: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 2, 0.0);
     case 113: return launch_cube_cfg<F, 2, 2, 1, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
     case 114: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 115: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 3, RP, 3, 2, true>(ctx, mode, s, qv, 1, 0.0);
-    case 116: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 3, RP, 2, 1, true>(ctx, mode, s, qv, 1, 0.0);
+    case 115: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 8, 1, false, 64>(ctx, mode, s, qv, 1, 0.0);
+    case 116: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.0);
     case 117: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
     case 118: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.0);
     default: return false;
