@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve (second half of the metric)")
+    p.add_argument("--no-c4", action="store_true", help="skip the short config-4 (largest single-GPU stencil) measurement")
     p.add_argument("--panel", type=int, default=0)
     p.add_argument("--variant", type=int, default=0)
     p.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
@@ -238,6 +239,42 @@ def end_to_end_solve(adp, configs, ctx, with_cpu: bool):
 
 
 # ------------------------------------------------------------- GPU arm ---
+def largest_config(adp, configs, ctx, peak):
+    """Config 4 (128^3 27-point stencil, q = 1024 fp64: 17.2 GB per block), a short device-resident
+    clenshaw_apply after the main measurement: the cube kernel (csrc/cheb_cube.cu) on its full panels.
+    Reported beside the headline, not part of it (its own operator, degree and timing)."""
+    import torch
+
+    cfg = configs.CONFIGS["c4"]
+    a = cfg.operator()
+    n, nnz, q = a.n_rows, a.nnz, cfg.q
+    k1 = configs.filter_degree(cfg)
+    f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, int(math.ceil(2.5 * k1)), 0.5)
+    da = adp.DeviceCsr(a, ctx)
+    x = torch.randn(n, q, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(0))
+    y = torch.empty_like(x)
+    deg = 24
+    adp.clenshaw_apply_device(f, da, x, 4, out=y)  # operator plans + workspace
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(2):
+        adp.clenshaw_apply_device(f, da, x, deg, out=y)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms_launch = ev0.elapsed_time(ev1) / (2 * deg)
+    b_step = step_bytes(n, nnz, q)
+    gbs = b_step / (ms_launch * 1e-3) / 1e9
+    da.close()
+    del x, y
+    torch.cuda.empty_cache()
+    return {"workload": f"c4: {cfg.description}; 2 x clenshaw_apply degree {deg}, inputs resident",
+            "n": n, "nnz": nnz, "q": q, "bytes_per_degree_step": b_step, "ms_per_degree_step": round(ms_launch, 4),
+            "value": round(gbs, 3), "unit": "GB/s", "frac_of_hbm_peak": round(gbs / peak, 4),
+            "kernel": "cheb_cube_kernel (csrc/cheb_cube.cu) on the full 64-vector panels"}
+
+
 def run_ours(args):
     import torch
 
@@ -357,6 +394,12 @@ def run_ours(args):
     if rank == 0 and not args.no_solve:
         solve_info = end_to_end_solve(adp, configs, ctx, with_cpu=(world == 1 and not args.no_cpu_baseline))
 
+    c4 = None
+    if rank == 0 and world == 1 and not args.no_c4 and args.config == "c2":
+        del x, y
+        torch.cuda.empty_cache()
+        c4 = largest_config(adp, configs, ctx, peaks()[0])
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sec, steps, threads = cpu_sample(a, q, args.cpu_seconds)
@@ -386,6 +429,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "solve": solve_info,
+            "largest_config": c4,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
