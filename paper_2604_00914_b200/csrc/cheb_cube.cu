@@ -285,6 +285,7 @@ struct CbArgs {
   uint32_t ldg_b, ldy_b, ldo_b;
   int32_t nblk, n_panels, n_groups, gp;  // gp: panels per task
   int32_t nrem;
+  int32_t valid_vec;  // 16-byte vectors of a row that exist (the last panel may be partial)
   int64_t goff;
   const int4* blk;
   const int32_t* pat_ptr;
@@ -540,6 +541,9 @@ __global__ void __launch_bounds__(NT, MINB)
   for (int32_t panel = pan0; panel < pan1; ++panel) {
     const uint32_t voff = static_cast<uint32_t>(panel) * kPB + lane * 16u;
     const char* gb = p.g + voff;
+    bool okc[CH];  // lanes past a ragged width: their tiles read zeros (TMA), they load and store nothing
+#pragma unroll
+    for (int c = 0; c < CH; ++c) okc[c] = static_cast<int32_t>(panel * 32 * CH + c * 32 + lane) < p.valid_vec;
     double2 acc[LW][R][CH];
 #pragma unroll
     for (int lw = 0; lw < LW; ++lw)
@@ -550,8 +554,9 @@ __global__ void __launch_bounds__(NT, MINB)
           if constexpr (kSpmmAcc) {
             bool ok;
             const int32_t r = row_of(half * LW + lw, i, ok);
-            acc[lw][i][c] = ok ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c)
-                               : make_double2(0.0, 0.0);
+            acc[lw][i][c] = ok && okc[c]
+                                ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c)
+                                : make_double2(0.0, 0.0);
           } else {
             acc[lw][i][c] = make_double2(0.0, 0.0);
           }
@@ -654,7 +659,7 @@ __global__ void __launch_bounds__(NT, MINB)
                   reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
 #pragma unroll
               for (int c = 0; c < CH; ++c) {
-                double2 wv = __ldg(src + 32 * c);
+                double2 wv = okc[c] ? __ldg(src + 32 * c) : make_double2(0.0, 0.0);
                 if constexpr (kFirst) wv = scale2(p.s2, wv);
                 acc[lw][i][c] = F::mac(acc[lw][i][c], v, wv);
               }
@@ -682,6 +687,7 @@ __global__ void __launch_bounds__(NT, MINB)
             char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
+              if (!okc[c]) continue;
               double2 own = make_double2(0.0, 0.0);
               if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
               double2 res;
@@ -724,7 +730,7 @@ template <class F, int CH, int R, int LY, int LZ, int MM, int S, class RP, int M
 bool launch_cube_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv, int gp, double min_regular) {
   constexpr int L = LY * LZ;
   const adp_csr* a = s.a;
-  if (qv % (32 * CH) != 0) return false;
+  if (qv < 32 * CH) return false;  // a ragged last panel runs masked; narrower blocks take other kernels
   const CubePlan* plan = get_cube_plan(const_cast<adp_csr*>(a), R, LY, LZ, MM, s.row_begin, s.row_end);
   if (!plan->valid || plan->regular_rows_frac < min_regular) return false;
   constexpr int kWarps = NT / 32;
@@ -742,7 +748,8 @@ bool launch_cube_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
   k.ldy_b = static_cast<uint32_t>((s.ld_y / epv) * 16);
   k.ldo_b = static_cast<uint32_t>((s.ld_out / epv) * 16);
   k.nblk = static_cast<int32_t>(plan->n_blocks);
-  k.n_panels = static_cast<int32_t>(qv / (32 * CH));
+  k.n_panels = static_cast<int32_t>((qv + 32 * CH - 1) / (32 * CH));
+  k.valid_vec = static_cast<int32_t>(qv);
   k.gp = std::max(1, std::min(gp, k.n_panels));
   k.n_groups = (k.n_panels + k.gp - 1) / k.gp;
   k.nrem = static_cast<int32_t>(plan->n_rem);

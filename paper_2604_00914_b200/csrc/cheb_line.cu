@@ -878,8 +878,12 @@ bool auto_line(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
   const adp_csr* a = s.a;
   const bool long_rows = a->nnz >= 12 * a->n_rows;
   if (!long_rows || a->dtype != ADP_F64 || ctx->panel_cols != 0) return false;
+  // the cube kernel where the operator has 3-D shifted blocks: every panel in one launch when the last
+  // panel is at least half full (masked), else its full panels and the line kernel's masked tail;
+  // without 3-D blocks the line kernel's full panels plus one masked launch for the rest
   const int64_t full = qv / 64 * 64, rem = qv - full;
-  if (full > 0) {  // full panels: the cube kernel where the operator has 3-D shifted blocks, else the line kernel
+  if (qv >= 64 && (rem == 0 || rem >= 32) && launch_cube_auto(ctx, mode, s, qv)) return true;
+  if (full > 0) {
     StepArgs t = s;
     t.q = full * 2;
     if (!launch_cube_auto(ctx, mode, t, full) && !launch_line_cfg<F, 2, 2, 3, RP, 3>(ctx, mode, t, full, 0.5))
@@ -918,7 +922,7 @@ bool launch_step_line(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
     // a row range (a rank's interior rows in the row-partitioned filter): the cube kernel plans its
     // blocks inside the range; the line kernel and ragged tails need whole operators
     return ctx->variant == 0 && !cplx && ctx->auto_line && a->nnz >= 12 * a->n_rows && ctx->panel_cols == 0 &&
-           qv % 64 == 0 && launch_cube_auto(ctx, mode, s, qv);
+           qv >= 64 && launch_cube_auto(ctx, mode, s, qv);
   }
   if (ctx->variant == 0) {
     if (cplx || !ctx->auto_line) return false;
