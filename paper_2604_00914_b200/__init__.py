@@ -12,6 +12,7 @@ from .filter import (ChebFilter, SpectrumBounds, adaptive_degree, build_filter, 
                      eval_filter_scalar, initial_degree, jackson_damping, lanczos_damping)
 from .operator import (Context, DeviceCsr, clenshaw_apply, clenshaw_apply_device, default_context, maspmm,
                        maspmm_device)
+from .hermitian import hermitian_embedding, solve_hermitian
 from .report import RunReport, dump_report, run_report_from_json, run_solve, to_json
 from .slicing import SlicedResult, balanced_slices, slice_interval, solve_sliced
 from .solver import (IterationRecord, SolveResult, SolverConfig, StageTimings, cholesky_qr_device,
@@ -21,7 +22,7 @@ from .sparse import (CsrMatrix, fill_gaussian, fill_rademacher, parse_matrix_mar
                      philox_gaussian, philox_uniform, read_matrix_market)
 
 __all__ = [
-    "SlicedResult", "balanced_slices", "slice_interval", "solve_sliced",
+    "SlicedResult", "balanced_slices", "slice_interval", "solve_sliced", "hermitian_embedding", "solve_hermitian",
     "RunReport", "dump_report", "run_report_from_json", "run_solve", "to_json",
     "c_m_constant", "damped_bound", "inspect_filter", "inspect_filter_csv", "j_theta", "projector_bound",
     "undamped_bound",

@@ -368,3 +368,27 @@ def test_solve_config1_window_matches_cpu_oracle(ctx, orc):
     assert np.all(np.abs(got.eigenvalues - want.eigenvalues) <= 1e-10 * np.abs(want.eigenvalues))
     scale = max(abs(got.bounds.lambda_min), abs(got.bounds.lambda_max))
     assert got.max_residual <= 1e-10 * scale * 1.01
+
+
+# ------------------------------------------------- complex Hermitian (configs 3, 5) ---
+def test_solve_hermitian_matches_dense(ctx):
+    # complex Hermitian eigenpairs through the real embedding (hermitian.py): a config-3-like Peierls
+    # lattice (24 x 24, phi = 1/8, on-site disorder) -- same count as the dense spectrum in the window,
+    # eigenvalues <= 1e-10 relative, residuals on H itself <= the solver tolerance.
+    from paper_2604_00914_b200 import configs
+
+    h = configs.peierls_lattice(24, phi=1.0 / 8.0, seed=3)
+    assert h.is_complex
+    sp = np.linalg.eigvalsh(h.to_dense())
+    lo, hi = 0.5 * (sp[280] + sp[281]), 0.5 * (sp[292] + sp[293])
+    got = adp.solve_hermitian(h, adp.SolverConfig(interval_a=lo, interval_b=hi, rng_seed=1), ctx)
+    assert got.converged
+    assert len(got.eigenvalues) == 12
+    scale = float(np.max(np.abs(sp)))
+    assert np.all(np.abs(got.eigenvalues - sp[281:293]) <= 1e-10 * scale)
+    assert got.eigenvectors.dtype == np.complex128 and got.eigenvectors.shape == (h.n_rows, 12)
+    hd = h.to_dense()
+    res = np.linalg.norm(hd @ got.eigenvectors - got.eigenvectors * got.eigenvalues, axis=0)
+    assert np.all(res <= 1e-9 * scale)
+    g = got.eigenvectors.conj().T @ got.eigenvectors
+    assert np.allclose(g, np.eye(12), atol=1e-10)
