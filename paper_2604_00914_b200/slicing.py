@@ -100,7 +100,8 @@ def solve_sliced(dev_csr, config, n_slices: int | None = None, slices=None, grou
                  overlap: float = 0.01, rtol: float = 1e-8) -> SlicedResult:
     """Solve config.interval_a..interval_b slice by slice and merge (see the module docstring).
 
-    ``solve_fn(dev_csr, cfg) -> SolveResult`` defaults to the GPU `solve`; tests inject a stand-in.
+    ``solve_fn(dev_csr, cfg) -> SolveResult`` defaults to the GPU `solve` (to `solve_hermitian` when
+    ``dev_csr`` is a complex host CsrMatrix: config 5's slices); tests inject a stand-in.
     Pairs found by two neighbouring slices inside their overlap (values within rtol x scale) are
     kept once; genuinely repeated eigenvalues are matched one to one, so multiplicities survive.
     """
@@ -109,7 +110,15 @@ def solve_sliced(dev_csr, config, n_slices: int | None = None, slices=None, grou
 
     from .solver import solve
 
-    solve_fn = solve_fn or solve
+    if solve_fn is None:
+        from .sparse import CsrMatrix
+
+        if isinstance(dev_csr, CsrMatrix) and dev_csr.is_complex:
+            from .hermitian import solve_hermitian
+
+            solve_fn = solve_hermitian
+        else:
+            solve_fn = solve
     a, b = float(config.interval_a), float(config.interval_b)
     if slices is None:
         slices = slice_interval(a, b, n_slices or 1)
