@@ -266,9 +266,19 @@ CONFIGS = {
     "c1s": Config("c1s", "3D 7-pt Laplacian 40^3 + U[0,1) potential, solve window ~35 eigenvalues", 64,
                   (0.425 * 13.0 - 0.002, 0.425 * 13.0 + 0.002), (0.0, 13.0), "f64",
                   lambda: laplacian7_potential(40, 0.0, 1.0)),
+    # bounds: the Gershgorin enclosure [-5.885, 8.533] (the 64 wells of depth 2 overlap down to -5.9;
+    # Lanczos: [-5.47, 6.16]). An earlier (-2.0, 8.6) missed the wells' bottom: the filter diverged at
+    # high degree (the trace estimate at k_max = 765 returned NaN); low-degree timings were unaffected.
     "c4": Config("c4", "3D 27-pt Mehrstellen 128^3 + Gaussian-sum potential, q=1024", 1024,
-                 (0.30, 0.32), (-2.0, 8.6), "f64",
+                 (0.30, 0.32), (-5.9, 8.6), "f64",
                  lambda: dft_like_27pt(128)),
+    # Config 4 for an END-TO-END solve on ONE GPU: "~1000 eigenpairs, block 1024" needs p = 1.8 e ~ 1840
+    # columns by the reference rule (six 2.1M x 1840 fp64 blocks = 185 GB, more than one B200 holds; the
+    # row-sharded 8-GPU layout is the configuration's own answer). This window holds ~510 eigenvalues
+    # (trace estimate: 851 in [0.30, 0.31]), so p ~ 920 fits one GPU.
+    "c4w": Config("c4w", "3D 27-pt Mehrstellen 128^3 + Gaussian-sum potential, solve window ~510 eigenvalues", 1024,
+                  (0.300, 0.306), (-5.9, 8.6), "f64",
+                  lambda: dft_like_27pt(128)),
     # Config 5 (n = 4e6, half-band 250, ~2.16 G nonzeros, complex128, q = 384) needs ~100 GB of host
     # memory just to assemble; c5s keeps its row structure (band 250 + 20 random off-band entries per
     # row, Re/Im ~ N(0, 1/2)) at n = 200,000 for tests and kernel measurements.
