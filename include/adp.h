@@ -71,23 +71,20 @@ void* adp_ctx_own_stream(const adp_ctx* ctx);
 adp_status adp_ctx_synchronize(adp_ctx* ctx);
 /* Number of kernels this library has launched on ctx (instrumentation for bench.py). */
 int64_t adp_ctx_launch_count(const adp_ctx* ctx);
+/* Kernel family of the last fused-step launch on ctx (1 row, 2 lean, 3 line, 4 cube,
+ * 5 plane sweep; 0 none yet) -- instrumentation for tests and bench.py. */
+int32_t adp_ctx_last_step_kernel(const adp_ctx* ctx);
 /* Kernel tuning knobs (0 = automatic): columns per warp task (panel width). */
 adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
-/* Kernel tuning variant of the fused step kernel (0 = automatic; see DESIGN.md
- * 3.1c). Every variant computes bit-identical results; they differ only in how
- * the gathered rows travel: 1-7 one-row-per-group kernel, 11-15 pipelined row
- * kernel, 21-24 row-block union, 31-33 deeper gather batches, 41-46 column
- * segments, 51-56 lane-parallel metadata, 61-66 shared-memory row window,
- * 71-76 two degree steps per launch, 81-91 and 98 line kernel (register reuse across
- * shifted-pattern row blocks), 92-97 line kernel with a TMA ring, 101-108 lean
- * kernel walking several rows per warp, 111-118 cube kernel (runs shared by 2-D/3-D
- * blocks of grid lines, TMA ring). Other values fail with
- * ADP_ERR_CONFIG. */
+/* Kernel family of the fused step kernel (0 = automatic). Every
+ * family computes bit-identical results; they differ only in how the gathered
+ * rows travel: 1 narrow-group row kernel, 2 lean kernel (one row per warp task),
+ * 3 line kernel (register reuse across shifted-pattern row blocks), 4 cube kernel
+ * (runs shared by 2-D/3-D blocks of grid lines), 5 plane-sweep stencil kernel
+ * (constant-coefficient 3-D stencils: halo tiles of W streamed plane by plane
+ * through shared memory). A family that does not apply to an operator falls
+ * back to the next one. Other values fail with ADP_ERR_CONFIG. */
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant);
-/* Tile-kernel knobs (0 = default): 16-byte vectors per lane per panel (1-4),
- * shared-memory pipeline stages, KiB per stage, resident CTAs per SM. */
-adp_status adp_ctx_set_tile_config(adp_ctx* ctx, int32_t chunks, int32_t stages, int32_t stage_kib,
-                                   int32_t ctas_per_sm);
 
 /* -------------------------------------------------------------- operator -- */
 /* Upload a CSR matrix (CsrMatrix, include/adapoly/csr_matrix.hpp:22-117: int64
@@ -110,6 +107,10 @@ adp_status adp_csr_create_device(adp_ctx* ctx, int64_t n_rows, int64_t n_cols, i
                                  const int32_t* d_col_idx, const void* d_values, adp_dtype dtype, adp_csr** out);
 adp_status adp_csr_destroy(adp_csr* a);
 adp_status adp_csr_info(const adp_csr* a, int64_t* n_rows, int64_t* n_cols, int64_t* nnz, int32_t* dtype);
+/* Whether the operator is a constant-coefficient radius-1 stencil on a structured grid
+ * (the plane-sweep kernel's precondition, verified entry by entry on first use):
+ * kind = 27 (box) or 7 (star) with dims = {nx, ny, nz}, else kind = 0. */
+adp_status adp_csr_stencil(adp_csr* a, int32_t* kind, int64_t* dims);
 
 /* clenshaw_apply (include/adapoly/cheb_filter.hpp:84-86, src/cheb_filter.cpp:129-179):
  * Y = rho(l(A)) X with host X / Y. coeffs = ChebFilter::coeffs (k_max+1 doubles),

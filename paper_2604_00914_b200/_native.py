@@ -86,9 +86,10 @@ SIGNATURES = {
     "adp_ctx_own_stream": (P, [P]),
     "adp_ctx_synchronize": (I32, [P]),
     "adp_ctx_launch_count": (I64, [P]),
+    "adp_ctx_last_step_kernel": (I32, [P]),
+    "adp_csr_stencil": (I32, [P, P, P]),
     "adp_ctx_set_panel": (I32, [P, I32]),
     "adp_ctx_set_tuning": (I32, [P, I32]),
-    "adp_ctx_set_tile_config": (I32, [P, I32, I32, I32, I32]),
     "adp_csr_create": (I32, [P, I64, I64, P, P, P, I32, P]),
     "adp_csr_create_device": (I32, [P, I64, I64, I64, P, P, P, I32, P]),
     "adp_csr_destroy": (I32, [P]),

@@ -31,18 +31,21 @@ def _assemble(n: int, cols: np.ndarray, vals: np.ndarray, valid: np.ndarray) -> 
     return CsrMatrix(n, n, row_ptr, np.ascontiguousarray(cols[valid], np.int64), np.ascontiguousarray(vals[valid]))
 
 
-def stencil_3d(nx: int, offsets, weights, diag: np.ndarray) -> CsrMatrix:
-    """Dirichlet stencil on an nx^3 grid (row = x + nx (y + nx z)); offsets in ascending linear order."""
-    n = nx ** 3
+def stencil_3d(nx: int, offsets, weights, diag: np.ndarray, ny: int | None = None, nz: int | None = None) -> CsrMatrix:
+    """Dirichlet stencil on an nx x ny x nz grid (default nx^3; row = x + nx (y + ny z)); offsets in
+    ascending linear order."""
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    n = nx * ny * nz
     idx = np.arange(n, dtype=np.int64)
-    x, y, z = idx % nx, (idx // nx) % nx, idx // (nx * nx)
+    x, y, z = idx % nx, (idx // nx) % ny, idx // (nx * ny)
     k = len(offsets)
     cols = np.empty((n, k), np.int64)
     vals = np.empty((n, k), np.float64)
     valid = np.empty((n, k), bool)
     for j, ((dx, dy, dz), w) in enumerate(zip(offsets, weights)):
-        ok = (x + dx >= 0) & (x + dx < nx) & (y + dy >= 0) & (y + dy < nx) & (z + dz >= 0) & (z + dz < nx)
-        cols[:, j] = idx + dx + nx * (dy + nx * dz)
+        ok = (x + dx >= 0) & (x + dx < nx) & (y + dy >= 0) & (y + dy < ny) & (z + dz >= 0) & (z + dz < nz)
+        cols[:, j] = idx + dx + nx * (dy + ny * dz)
         if (dx, dy, dz) == (0, 0, 0):
             vals[:, j] = diag
         else:

@@ -64,69 +64,17 @@ struct adp_ctx {
   int sm_count = 148;
   int64_t launches = 0;
   int panel_cols = 0;  // 0 = automatic
-  int variant = 0;     // kernel tuning variant (0 = automatic; 1-7 one-row-per-warp kernel; 11-15 pipelined)
-  int pipe_variant = 0;  // derived: variant - 10 for the pipelined row kernel
-  // tile kernel knobs (0 = default): chunks per lane, pipeline stages, stage KiB, CTAs per SM
-  int tile_ch = 0, tile_stages = 0, tile_stage_kb = 0, tile_ctas = 0;
-  int pair_variant = 0;  // two-step (pair) kernel geometry; 0 = off
-  adp::DevBuf sched;      // task tickets of persistent kernels (self re-arming)
+  int variant = 0;     // kernel family (adp_ctx_set_tuning): 0 automatic, 1 row, 2 lean, 3 line, 4 cube, 5 sweep
   bool pdl = true;        // programmatic dependent launch between degree steps (ADP_NO_PDL=1: off)
   bool auto_line = true;  // automatic line-kernel choice (ADP_NO_LINE=1: off, for A/B timing)
   bool auto_cube = true;  // automatic cube-kernel choice for its full panels (ADP_NO_CUBE=1: off)
-  bool sched_ready = false;
+  bool auto_sweep = true; // automatic plane-sweep stencil kernel (ADP_NO_SWEEP=1: off)
+  int last_kernel = 0;    // family of the last step launch (adp_ctx_last_step_kernel)
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;
   void* cusolver = nullptr;
   int* halo_failed = nullptr;  // set by the halo wait kernel on timeout (adp_halo_check)
 };
-
-namespace adp {
-constexpr int64_t kMaxTileRows = 64;
-constexpr int64_t kMaxTileDistinct = 256;  // = 32 lanes x kMaxDPerLane (cheb_tile.cu)
-
-// Row tiling of a CSR operator for one (panel width, stage size) pair (tiling.cpp).
-struct Tiling {
-  int64_t panel_bytes = 0, stage_bytes = 0;
-  bool ok = false;
-  int64_t n_tiles = 0, max_rows = 0, distinct = 0;
-  void* d_tile_row = nullptr;   // int32[T+1]
-  void* d_tile_dptr = nullptr;  // int64[T+1]
-  void* d_tile_blob = nullptr;  // int64[T+1] byte offsets into d_blob
-  void* d_dcol = nullptr;       // int32[distinct]
-  void* d_blob = nullptr;       // per-tile metadata blobs
-  ~Tiling();
-};
-}  // namespace adp
-
-namespace adp {
-// Column-segment layout of R-row blocks (segments.cpp): the reference's
-// TiledMatrix (tiled_matrix.hpp:23-94) with T_i = R -- per row block, the
-// ascending DISTINCT columns its rows touch, a bitmask of the rows that hold
-// each one, and the R values (0 where absent). Used by cheb_seg_kernel.
-struct Segments {
-  int rows_per_block = 0;
-  int64_t n_blocks = 0, n_segs = 0;
-  void* d_blk_ptr = nullptr;  // int64[n_blocks+1]
-  void* d_col = nullptr;      // int32[n_segs]
-  void* d_mask = nullptr;     // uint32[n_segs] (bit i: row i of the block has the column)
-  void* d_val = nullptr;      // Scalar[n_segs * R]
-  double reuse = 0.0;         // nnz / n_segs
-  ~Segments();
-};
-}  // namespace adp
-
-namespace adp {
-// Chunk dependency plan of an operator for the two-step pair kernel (cheb_pair.cu).
-struct PairPlan {
-  int64_t chunk_rows = 0, gs = 0, nch = 0, ngroups = 0, reach = 0;
-  void* d_glo = nullptr;       // int32[nch]: first counter group a step-(j-1) chunk waits on
-  void* d_ghi = nullptr;       // int32[nch]: last one
-  void* d_counters = nullptr;  // uint32[counter_panels * ngroups], cumulative completion counts
-  int64_t counter_panels = 0;
-  uint32_t epoch = 0;
-  ~PairPlan();
-};
-}  // namespace adp
 
 namespace adp {
 // Shifted-pattern row blocks of an operator for the line kernel (cheb_line.cu).
@@ -165,6 +113,24 @@ struct CubePlan {
 };
 }  // namespace adp
 
+namespace adp {
+// A constant-coefficient stencil on a structured grid (cheb_sweep.cu): row r is grid point
+// (x, y, z) = (r % nx, (r / nx) % ny, r / (nx ny)); its columns are the in-grid points of a fixed
+// radius-1 offset set (the 27-point box or the 7-point star) in ascending order, and every row holds
+// the same value at each offset except the centre (the diagonal: a potential), which is per row.
+// Detected and verified entry by entry against the CSR once per operator; a lossless re-encoding.
+struct StencilPlan {
+  bool valid = false;
+  int kind = 0;               // 27 (box) or 7 (star)
+  int64_t nx = 0, ny = 0, nz = 0;
+  int64_t nxp = 0;            // x pitch of the diagonal array (even: 16-byte rows for TMA)
+  double w[27] = {};          // value at offset (dx, dy, dz): index (dz+1)*9 + (dy+1)*3 + (dx+1); centre unused
+  double* d_diag = nullptr;   // [nz][ny][nxp] centre values
+  std::string why;            // why the operator is not such a stencil (diagnostics)
+  ~StencilPlan();
+};
+}  // namespace adp
+
 struct adp_csr {
   adp_ctx* ctx = nullptr;     // creating context (must outlive every call that uses this operator)
   int device = 0;             // destroy needs only this: the operator may outlive its context
@@ -179,11 +145,9 @@ struct adp_csr {
   std::vector<int32_t> h_col;
   void* h_values = nullptr;  // malloc'd copy of the values
   bool host_ready = false;   // h_* filled (eagerly by adp_csr_create, lazily for device-created operators)
-  std::vector<std::unique_ptr<adp::Tiling>> tilings;
-  std::vector<std::unique_ptr<adp::Segments>> segments;
-  std::vector<std::unique_ptr<adp::PairPlan>> pair_plans;
   std::vector<std::unique_ptr<adp::LinePlan>> line_plans;
   std::vector<std::unique_ptr<adp::CubePlan>> cube_plans;
+  std::unique_ptr<adp::StencilPlan> stencil;  // built on first use (cheb_sweep.cu)
 };
 
 namespace adp {
@@ -257,32 +221,8 @@ void launch_scale_rows(adp_ctx* ctx, const void* src, int64_t lds, void* dst, in
 void launch_fill_philox(adp_ctx* ctx, double* dst, int64_t n, int64_t q, int64_t ld, uint64_t seed,
                         uint64_t stream, int kind);
 
-// Tiling (tiling.cpp) and the TMA-pipelined tile kernel (cheb_tile.cu).
-int64_t tile_blob_bytes(int64_t rows, int64_t nnz_t, int64_t val_bytes);
-const Tiling* get_tiling(adp_csr* a, int64_t panel_bytes, int64_t stage_bytes);
-// Launches the tiled kernel for the step; returns false if the operator cannot
-// be tiled for this width (the caller then uses the row kernel).
-bool launch_step_tiled(adp_ctx* ctx, StepMode mode, const StepArgs& args);
-// The persistent software-pipelined row kernel (cheb_row.cu; tuning variants).
-bool launch_step_row(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 // The default lean kernel (cheb_lean.cu) for >= 4 vectors per row.
 bool launch_step_lean(adp_ctx* ctx, StepMode mode, const StepArgs& args);
-
-// Two consecutive in-place Clenshaw steps in one launch (cheb_pair.cu): step j
-// reads g (gathered), v, y and writes v; step j-1 gathers that v, reads g and y
-// and writes out (== g in place, or the final output). Returns false when the
-// pair kernel is off or does not apply; the caller then runs two single steps.
-struct PairStep {
-  const void* g;
-  void* v;
-  const void* y;
-  void* out;
-  int64_t ld, ld_y, ld_out;  // elements
-  double f0, f1, f2;         // step j scalars
-  double b0, b1, b2;         // step j-1 scalars
-};
-bool launch_pair(adp_ctx* ctx, const adp_csr* a, const PairStep& ps, int64_t q);
-PairPlan* get_pair_plan(adp_csr* a, int64_t chunk_rows, int64_t gs, int64_t n_panels);
 
 // The line kernel (cheb_line.cu): register reuse of gathered rows across
 // blocks of rows with shifted column patterns. Returns false if not applicable.
@@ -293,6 +233,10 @@ bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& args, int64_t vectors);
 const CubePlan* get_cube_plan(adp_csr* a, int rows_per_line, int ly, int lz, int max_run, int64_t row_begin,
                               int64_t row_end);
+// The plane-sweep stencil kernel (cheb_sweep.cu): Step launches on constant-coefficient 3-D stencil
+// operators (StencilPlan). Returns false if not applicable.
+bool launch_step_sweep(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+const StencilPlan* get_stencil_plan(adp_csr* a);
 // Host copies of a device-created operator's arrays, downloaded on first use by the
 // host-side preprocessing (line plans, tilings, segments, the dense fallback).
 void ensure_host_copy(adp_csr* a);
@@ -305,9 +249,6 @@ inline void plan_uploads_done() { ADP_CUDA(cudaStreamSynchronize(cudaStreamLegac
 int validate_csr_device(adp_ctx* ctx, const int64_t* row_ptr, const int32_t* col, int64_t n_rows, int64_t n_cols,
                         int64_t nnz);
 void narrow_row_ptr_device(adp_ctx* ctx, const int64_t* src, int32_t* dst, int64_t count);
-
-// Column segments of R-row blocks (segments.cpp); built once per (operator, R).
-const Segments* get_segments(adp_csr* a, int rows_per_block);
 
 // Host filter helpers (filter_host.cpp).
 std::vector<double> step_coeffs(double alpha, double beta, int k);

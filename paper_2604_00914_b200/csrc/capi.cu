@@ -107,46 +107,7 @@ void clenshaw_device(adp_ctx* ctx, const adp_csr* a, const double* coeffs, doubl
     t[2] = coeffs[j];
   };
   int j = deg - 2;
-  // With the pair kernel (cheb_pair.cu) steps run two per launch; an odd count
-  // runs its first step alone.
-  if (ctx->pair_variant != 0 && (j + 1) % 2 == 1 && j >= 1) {
-    s.gsrc = cur_w;
-    s.vin = cur_v;
-    s.out = cur_v;
-    s.ld_out = ld;
-    double t[3];
-    scalars(j, t);
-    s.s0 = t[0];
-    s.s1 = t[1];
-    s.s2 = t[2];
-    launch_step(ctx, StepMode::Step, s);
-    std::swap(cur_w, cur_v);
-    --j;
-  }
   for (; j >= 0; --j) {
-    if (ctx->pair_variant != 0 && j >= 1) {
-      PairStep ps{};
-      ps.g = cur_w;
-      ps.v = cur_v;
-      ps.y = y;
-      ps.out = j - 1 == 0 ? out : cur_w;
-      ps.ld = ld;
-      ps.ld_y = ld_y;
-      ps.ld_out = j - 1 == 0 ? ld_out : ld;
-      double t[3];
-      scalars(j, t);
-      ps.f0 = t[0];
-      ps.f1 = t[1];
-      ps.f2 = t[2];
-      scalars(j - 1, t);
-      ps.b0 = t[0];
-      ps.b1 = t[1];
-      ps.b2 = t[2];
-      if (launch_pair(ctx, a, ps, q)) {  // b_j in cur_v, b_{j-1} in cur_w (or out)
-        --j;
-        continue;
-      }
-    }
     s.gsrc = cur_w;
     s.vin = cur_v;
     s.out = j == 0 ? out : cur_v;
@@ -236,6 +197,8 @@ adp_status adp_ctx_create(int32_t device, adp_ctx** out) {
     ctx->auto_line = !(no_line && no_line[0] == '1');
     const char* no_cube = std::getenv("ADP_NO_CUBE");
     ctx->auto_cube = !(no_cube && no_cube[0] == '1');
+    const char* no_sweep = std::getenv("ADP_NO_SWEEP");
+    ctx->auto_sweep = !(no_sweep && no_sweep[0] == '1');
     *out = ctx;
   });
 }
@@ -249,7 +212,6 @@ adp_status adp_ctx_destroy(adp_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     adp_release_dense_handles(ctx);
     for (auto& b : ctx->ws) b.release();
-    ctx->sched.release();
     if (ctx->halo_failed) cudaFree(ctx->halo_failed);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
@@ -273,6 +235,20 @@ adp_status adp_ctx_synchronize(adp_ctx* ctx) {
 
 int64_t adp_ctx_launch_count(const adp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int32_t adp_ctx_last_step_kernel(const adp_ctx* ctx) { return ctx ? ctx->last_kernel : 0; }
+
+adp_status adp_csr_stencil(adp_csr* a, int32_t* kind, int64_t* dims) {
+  return guarded([&] {
+    if (!a || !kind || !dims) fail(ADP_ERR_CONFIG, "adp_csr_stencil: null argument");
+    set_device(a->ctx);
+    const adp::StencilPlan* p = a->dtype == ADP_F64 && a->nnz <= 27 * a->n_rows ? adp::get_stencil_plan(a) : nullptr;
+    *kind = p && p->valid ? p->kind : 0;
+    dims[0] = p && p->valid ? p->nx : 0;
+    dims[1] = p && p->valid ? p->ny : 0;
+    dims[2] = p && p->valid ? p->nz : 0;
+  });
+}
+
 adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
   return guarded([&] {
     if (panel_cols < 0) fail(ADP_ERR_CONFIG, "adp_ctx_set_panel: negative panel width");
@@ -282,28 +258,9 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
 
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
   return guarded([&] {
-    // 0 auto; 1-7 one-row kernel; 11-15 pipelined row kernel; 21-24 union; 31-33 deep batches; 41-46 segments
-    if (variant < 0 || (variant > 7 && variant < 11) || (variant > 15 && variant < 21) ||
-        (variant > 24 && variant < 31) || (variant > 33 && variant < 40) || (variant > 49 && variant < 51) ||
-        (variant > 56 && variant < 61) || (variant > 66 && variant < 71) || (variant > 76 && variant < 81) ||
-        (variant > 98 && variant < 101) || (variant > 108 && variant < 111) || variant > 118)
-      fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
+    // 0 automatic; 1-5 force one kernel family (adp.h)
+    if (variant < 0 || variant > 5) fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
-    ctx->pair_variant = (variant > 70 && variant < 77) ? variant - 70 : 0;
-    ctx->pipe_variant = (variant > 10 && variant < 16) ? variant - 10 : 0;
-  });
-}
-
-adp_status adp_ctx_set_tile_config(adp_ctx* ctx, int32_t chunks, int32_t stages, int32_t stage_kib,
-                                   int32_t ctas_per_sm) {
-  return guarded([&] {
-    if (chunks < 0 || chunks > 4 || stages < 0 || stages > 8 || stage_kib < 0 || stage_kib > 220 ||
-        ctas_per_sm < 0 || ctas_per_sm > 4)
-      fail(ADP_ERR_CONFIG, "adp_ctx_set_tile_config: knob out of range");
-    ctx->tile_ch = chunks;
-    ctx->tile_stages = stages;
-    ctx->tile_stage_kb = stage_kib;
-    ctx->tile_ctas = ctas_per_sm;
   });
 }
 

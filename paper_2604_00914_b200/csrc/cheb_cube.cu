@@ -792,22 +792,6 @@ bool launch_cube_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
   return true;
 }
 
-// tuning variants 111-118: <CH, R, LY, LZ, MM, RP, MINB>, panels per task
-template <class F, class RP>
-bool dispatch_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
-  switch (ctx->variant) {
-    // <CH, R, LY, LZ, MM, S, RP, MINB>, panels per task
-    case 111: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 3, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 112: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 2, 0.0);
-    case 113: return launch_cube_cfg<F, 2, 2, 1, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 114: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 115: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 8, 1, false, 64>(ctx, mode, s, qv, 1, 0.0);
-    case 116: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.0);
-    case 117: return launch_cube_cfg<F, 2, 2, 2, 1, 3, 2, RP, 2>(ctx, mode, s, qv, 1, 0.0);
-    case 118: return launch_cube_cfg<F, 2, 2, 2, 2, 3, 2, RP, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.0);
-    default: return false;
-  }
-}
 
 }  // namespace
 
@@ -821,16 +805,14 @@ bool launch_cube_auto(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv
 }
 
 bool launch_step_cube(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
+  // variant 4: the cube kernel forced on any real operator (its automatic geometry, no regularity floor)
   const adp_csr* a = s.a;
-  if (ctx->variant < 111 || ctx->variant > 118) return false;
-  if (a->n_rows >= (int64_t{1} << 30)) return false;
-  const bool cplx = a->dtype == ADP_C128;
-  const int epv = cplx ? 1 : 2;
-  const int64_t qv = (s.q + epv - 1) / epv;
+  if (ctx->variant != 4 || a->dtype != ADP_F64 || a->n_rows >= (int64_t{1} << 30)) return false;
+  const int64_t qv = (s.q + 1) / 2;
   for (int64_t ld : {s.ld, s.ld_y, s.ld_out})
-    if (ld % epv != 0 || (ld / epv) * 16 >= (int64_t{1} << 32)) return false;
-  if (cplx) return a->rp64 ? dispatch_cube<CplxC, int64_t>(ctx, mode, s, qv) : dispatch_cube<CplxC, int32_t>(ctx, mode, s, qv);
-  return a->rp64 ? dispatch_cube<RealC, int64_t>(ctx, mode, s, qv) : dispatch_cube<RealC, int32_t>(ctx, mode, s, qv);
+    if (ld % 2 != 0 || (ld / 2) * 16 >= (int64_t{1} << 32)) return false;
+  return a->rp64 ? launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int64_t, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.0)
+                 : launch_cube_cfg<RealC, 2, 2, 2, 2, 3, 2, int32_t, 4, 1, false, 128>(ctx, mode, s, qv, 1, 0.0);
 }
 
 }  // namespace adp

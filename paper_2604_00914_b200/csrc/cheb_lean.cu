@@ -302,850 +302,11 @@ void launch_lean(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
   ctx->launches += 1;
 }
 
-// ---- multi-row lean kernel ---------------------------------------------------------------
-// cheb_lean_kernel's arithmetic and data movement, but each group walks RPW rows
-// of its panel instead of one: the prologue (task decomposition, mbarrier init,
-// cache policy) is paid once per RPW rows, the next row's row_ptr entry is the
-// current row's end, and the next row's V / Y panels are bulk-copied into the
-// group's (single) slot as soon as the epilogue has read it, so they land while
-// the next row's gathers are in flight. STRD: the CTA's groups take rows
-// rb + i*kGroups + grp (the 8 warps of a CTA work on 8 consecutive rows at any
-// time, as in the one-row kernel, sharing x-neighbour gathers through L1);
-// otherwise rows rb + grp*RPW + i (each warp re-gathers its previous row's
-// neighbours). Rows are independent, so every bit of the result is unchanged.
-template <class F, int G, int CH, int RPW, bool STRD, int MODE, class RP, int MINB, bool MASK = false>
-__global__ void __launch_bounds__(kThreads, MINB) cheb_leanm_kernel(const LArgs p) {
-  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
-  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
-  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
-  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
-  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
-  constexpr int kGroups = kThreads / G;
-  constexpr int kRowsPerCta = kGroups * RPW;
-  constexpr uint32_t kPB = G * CH * 16u;
-  extern __shared__ __align__(16) uint8_t smem[];
-
-  const int grp = threadIdx.x / G, lane = threadIdx.x % G;
-  const uint32_t gmask = G == 32 ? 0xffffffffu : (((1u << (G % 32)) - 1u) << ((threadIdx.x % 32) / G * G));
-  const int32_t nrows = static_cast<int32_t>(p.nrows);
-  const int32_t nblk = (nrows + kRowsPerCta - 1) / kRowsPerCta;
-  const int32_t panel = static_cast<int32_t>(blockIdx.x) / nblk;  // CTA-uniform
-  const int32_t rb = (static_cast<int32_t>(blockIdx.x) - panel * nblk) * kRowsPerCta;
-  auto rel_row = [&](int i) -> int32_t { return STRD ? rb + i * kGroups + grp : rb + grp * RPW + i; };
-  int32_t rel = rel_row(0);
-  if (rel >= nrows) return;  // group-uniform
-  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
-  const uint32_t voff = poff + lane * 16u;
-  const uint64_t pol = policy_evict_first(1.0f);
-
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + grp;
-  double2* my = reinterpret_cast<double2*>(smem + ((kGroups * 8 + 15) / 16) * 16) + grp * (2 * G * CH);
-  int64_t r = p.row_begin + rel;
-  RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r));
-  RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r + 1));
-  pdl_wait_and_release();
-  bool ok[CH];
-#pragma unroll
-  for (int c = 0; c < CH; ++c) ok[c] = !MASK || c * G + lane < p.valid;
-  const uint32_t cpb = MASK ? static_cast<uint32_t>(p.valid) * 16u : kPB;
-  if constexpr (kStep) {
-    if (lane == 0) {
-      mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      mbar_arrive_expect_tx(bar, 2 * cpb);
-      bulk_g2s_hint(my, p.vin + static_cast<uint64_t>(r) * p.ldg_b + poff, cpb, bar, pol);
-      bulk_g2s_hint(my + G * CH, p.yin + static_cast<uint64_t>(r) * p.ldy_b + poff, cpb, bar, pol);
-    }
-  }
-  const char* gb = p.g + voff;
-  uint32_t phase = 0;
-#pragma unroll 1
-  for (int i = 0; i < RPW; ++i) {
-    char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
-    double2 acc[CH];
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      if constexpr (kSpmmAcc)
-        acc[c] = ok[c] ? *reinterpret_cast<const double2*>(ob + G * 16 * c) : make_double2(0.0, 0.0);
-      else
-        acc[c] = make_double2(0.0, 0.0);
-    }
-    for (RP e = start; e < end; ++e) {
-      const int cidx = __ldg(p.col + e);
-      const auto v = F::load(p.val, static_cast<int64_t>(e));
-      const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
-      double2 w[CH];
-#pragma unroll
-      for (int c = 0; c < CH; ++c) w[c] = ok[c] ? __ldg(src + G * c) : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        double2 wv = w[c];
-        if constexpr (kFirst) wv = scale2(p.s2, wv);
-        acc[c] = F::mac(acc[c], v, wv);
-      }
-    }
-    // next row of this group (its row_ptr end is loaded before the epilogue's stores)
-    const int32_t nrel = i + 1 < RPW ? rel_row(i + 1) : nrows;
-    const bool more = nrel < nrows;
-    if (more) {
-      start = end;
-      if (STRD) start = static_cast<RP>(ld_rp<RP>(p.row_ptr, p.row_begin + nrel));
-      end = static_cast<RP>(ld_rp<RP>(p.row_ptr, p.row_begin + nrel + 1));
-    }
-    if constexpr (kStep) {
-      __syncwarp(gmask);
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-    }
-    const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
-    char* wb = kFirst ? p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff : nullptr;
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      if (!ok[c]) continue;
-      double2 own = make_double2(0.0, 0.0);
-      if constexpr (kNeedOwn) own = __ldg(own_src + G * c);
-      double2 res;
-      if constexpr (kStep) {
-        const double2 vv = my[c * G + lane];
-        const double2 yy = my[G * CH + c * G + lane];
-        res = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
-      } else if constexpr (kFirst) {
-        const double2 wn = scale2(p.s2, own);
-        st_hint(wb + G * 16 * c, wn, pol);
-        res = add2(scale2(p.s0, acc[c]), scale2(p.s1, wn));
-      } else if constexpr (kDeg1) {
-        res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own))));
-      } else {
-        res = acc[c];
-      }
-      st_hint(ob + G * 16 * c, res, pol);
-    }
-    if (!more) break;  // group-uniform
-    r = p.row_begin + nrel;
-    if constexpr (kStep) {
-      // the slot is free once every lane of the group has read it: refill it with the next row
-      __syncwarp(gmask);
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        mbar_arrive_expect_tx(bar, 2 * cpb);
-        bulk_g2s_hint(my, p.vin + static_cast<uint64_t>(r) * p.ldg_b + poff, cpb, bar, pol);
-        bulk_g2s_hint(my + G * CH, p.yin + static_cast<uint64_t>(r) * p.ldy_b + poff, cpb, bar, pol);
-      }
-    }
-  }
-}
-
-template <class F, int G, int CH, int RPW, bool STRD, class RP, int MINB, bool MASK = false>
-void launch_leanm(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
-  constexpr int kGroups = kThreads / G;
-  k.n_panels = MASK ? 1 : qv / (G * CH);
-  k.valid = static_cast<int32_t>(qv);
-  const int64_t nblk = (k.nrows + kGroups * RPW - 1) / (kGroups * RPW);
-  const int64_t grid64 = nblk * k.n_panels;
-  if (grid64 >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_leanm: too many CTAs");
-  const int grid = static_cast<int>(grid64);
-  const size_t smem = mode == StepMode::Step
-                          ? static_cast<size_t>((kGroups * 8 + 15) / 16) * 16 + static_cast<size_t>(kGroups) * 2 * G * CH * 16
-                          : 16;
-  auto run = [&](auto kern) {
-    if (smem > 48 * 1024)
-      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    launch_pdl(ctx, kern, dim3(grid), dim3(kThreads), smem, k);
-  };
-  switch (mode) {
-    case StepMode::First: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 0, RP, MINB, MASK>); break;
-    case StepMode::Step: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 1, RP, MINB, MASK>); break;
-    case StepMode::Deg1: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 2, RP, MINB, MASK>); break;
-    case StepMode::Spmm: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 3, RP, MINB, MASK>); break;
-    case StepMode::SpmmAcc: run(cheb_leanm_kernel<F, G, CH, RPW, STRD, 4, RP, MINB, MASK>); break;
-  }
-  ADP_LAUNCH_CHECK();
-  ctx->launches += 1;
-}
-
-// ---- row-block union kernel -----------------------------------------------------------
-// A warp owns R consecutive rows of one panel and walks the UNION of their
-// column sets in ascending order: every distinct W row panel is gathered once
-// and fed to each of the R rows that contain it (the reference's column
-// segments of a row block, tiled_matrix.hpp:78-91, done in registers). Each
-// row still sees its own entries in ascending column order, so the arithmetic
-// -- and every bit of the result -- is unchanged; the L1/L2 gather traffic
-// drops by the operator's intra-block column overlap (27-point stencil, R = 4:
-// 54 instead of 108 row-panel loads). Each row keeps its current and next
-// (col, val) in registers so the union minimum never waits on a load.
-template <class F, int CH, int R, int MODE, class RP, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) cheb_union_kernel(const LArgs p) {
-  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
-  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
-  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
-  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
-  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
-  constexpr int kWarps = kThreads / 32;
-  constexpr uint32_t kPB = 32 * CH * 16u;
-  constexpr int kNone = 0x7fffffff;
-  using Val = typename F::Val;
-  extern __shared__ __align__(16) uint8_t smem[];  // [8 mbarriers][warp][row][V, Y] panels
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int32_t nrows = static_cast<int32_t>(p.nrows);
-  const int32_t nblk = (nrows + R - 1) / R;
-  const int32_t task = static_cast<int32_t>(blockIdx.x) * kWarps + warp;
-  if (task >= nblk * static_cast<int32_t>(p.n_panels)) return;
-  const int32_t panel = task / nblk;
-  const int32_t b = task - panel * nblk;
-  const int64_t r0 = p.row_begin + static_cast<int64_t>(b) * R;
-  const int rows = min(R, nrows - b * R);
-  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
-  const uint32_t voff = poff + lane * 16u;
-  const uint64_t pol = policy_evict_first(1.0f);
-
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
-  double2* my = reinterpret_cast<double2*>(smem + 128) + warp * (R * 2 * 32 * CH);
-  if constexpr (kStep) {
-    if (lane == 0) {
-      mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      mbar_arrive_expect_tx(bar, 2 * kPB * rows);
-    }
-    __syncwarp();
-    if (lane < rows) {
-      bulk_g2s_hint(my + lane * (2 * 32 * CH), p.vin + static_cast<uint64_t>(r0 + lane) * p.ldg_b + poff, kPB, bar, pol);
-      bulk_g2s_hint(my + lane * (2 * 32 * CH) + 32 * CH, p.yin + static_cast<uint64_t>(r0 + lane) * p.ldy_b + poff, kPB,
-                    bar, pol);
-    }
-  }
-  const char* gb = p.g + voff;
-
-  RP k[R], e[R];
-  int c0[R], c1[R];
-  Val v0[R], v1[R];
-  double2 acc[R][CH];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    k[i] = 0;
-    e[i] = 0;
-    if (i < rows) {
-      k[i] = static_cast<RP>(ld_rp<RP>(p.row_ptr, r0 + i));
-      e[i] = static_cast<RP>(ld_rp<RP>(p.row_ptr, r0 + i + 1));
-    }
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      if constexpr (kSpmmAcc)
-        acc[i][c] = i < rows ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r0 + i) * p.ldo_b + voff + 512 * c)
-                             : make_double2(0.0, 0.0);
-      else
-        acc[i][c] = make_double2(0.0, 0.0);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    c0[i] = k[i] < e[i] ? __ldg(p.col + k[i]) : kNone;
-    v0[i] = k[i] < e[i] ? F::load(p.val, k[i]) : Val{};
-    c1[i] = k[i] + 1 < e[i] ? __ldg(p.col + k[i] + 1) : kNone;
-    v1[i] = k[i] + 1 < e[i] ? F::load(p.val, k[i] + 1) : Val{};
-  }
-  while (true) {
-    int cmin = c0[0];
-#pragma unroll
-    for (int i = 1; i < R; ++i) cmin = min(cmin, c0[i]);
-    if (cmin == kNone) break;
-    double2 w[CH];
-    const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cmin)) * p.ldg_b);
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      w[c] = __ldg(src + 32 * c);
-      if constexpr (kFirst) w[c] = scale2(p.s2, w[c]);
-    }
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      if (c0[i] == cmin) {
-#pragma unroll
-        for (int c = 0; c < CH; ++c) acc[i][c] = F::mac(acc[i][c], v0[i], w[c]);
-        ++k[i];
-        c0[i] = c1[i];
-        v0[i] = v1[i];
-        c1[i] = k[i] + 1 < e[i] ? __ldg(p.col + k[i] + 1) : kNone;
-        v1[i] = k[i] + 1 < e[i] ? F::load(p.val, k[i] + 1) : Val{};
-      }
-    }
-  }
-  if constexpr (kStep) {
-    __syncwarp();
-    mbar_wait(bar, 0);
-  }
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    if (i >= rows) break;
-    const int64_t r = r0 + i;
-    const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
-    char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      double2 own = make_double2(0.0, 0.0);
-      if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
-      double2 res;
-      if constexpr (kStep) {
-        const double2 vv = my[i * (2 * 32 * CH) + c * 32 + lane];
-        const double2 yy = my[i * (2 * 32 * CH) + 32 * CH + c * 32 + lane];
-        res = add2(sub2(add2(scale2(p.s0, acc[i][c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
-      } else if constexpr (kFirst) {
-        const double2 wn = scale2(p.s2, own);
-        st_hint(p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c, wn, pol);
-        res = add2(scale2(p.s0, acc[i][c]), scale2(p.s1, wn));
-      } else if constexpr (kDeg1) {
-        res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[i][c]), scale2(p.s3, own))));
-      } else {
-        res = acc[i][c];
-      }
-      st_hint(ob + 512 * c, res, pol);
-    }
-  }
-}
-
-template <class F, int CH, int R, class RP, int MINB>
-void launch_union(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
-  constexpr int kWarps = kThreads / 32;
-  k.n_panels = qv / (32 * CH);
-  const int64_t nblk = (k.nrows + R - 1) / R;
-  const int64_t total = nblk * k.n_panels;
-  if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_union: too many tasks");
-  const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
-  const size_t smem = mode == StepMode::Step ? 128 + static_cast<size_t>(kWarps) * R * 2 * 32 * CH * 16 : 16;
-  auto run = [&](auto kern) {
-    if (smem > 48 * 1024)
-      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, kThreads, smem, ctx->stream>>>(k);
-  };
-  switch (mode) {
-    case StepMode::First: run(cheb_union_kernel<F, CH, R, 0, RP, MINB>); break;
-    case StepMode::Step: run(cheb_union_kernel<F, CH, R, 1, RP, MINB>); break;
-    case StepMode::Deg1: run(cheb_union_kernel<F, CH, R, 2, RP, MINB>); break;
-    case StepMode::Spmm: run(cheb_union_kernel<F, CH, R, 3, RP, MINB>); break;
-    case StepMode::SpmmAcc: run(cheb_union_kernel<F, CH, R, 4, RP, MINB>); break;
-  }
-  ADP_LAUNCH_CHECK();
-  ctx->launches += 1;
-}
-
-// ---- lean kernel with lane-parallel metadata ----------------------------------------------
-// As cheb_lean_kernel (G = 32), but the row's (col, val) window is fetched with
-// one coalesced load (lane k holds entry k) and broadcast by shuffles, so the W
-// gathers depend on no memory load and U of them are issued back to back --
-// removes the per-nonzero (col load -> W load) latency chain of long rows
-// (27-point stencil, config 4).
-template <class F, int CH, int U, int MODE, class RP, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) cheb_lean2_kernel(const LArgs p) {
-  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
-  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
-  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
-  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
-  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
-  constexpr int kWarps = kThreads / 32;
-  constexpr uint32_t kPB = 32 * CH * 16u;
-  using Val = typename F::Val;
-  extern __shared__ __align__(16) uint8_t smem[];
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int32_t nrows = static_cast<int32_t>(p.nrows);
-  int32_t task = static_cast<int32_t>(blockIdx.x) * kWarps + warp;
-  const bool live = task < nrows * static_cast<int32_t>(p.n_panels);
-  if (!live) task = 0;  // no early return: keeps the warp provably converged at the shuffles
-  const int32_t panel = task / nrows;
-  const int64_t r = p.row_begin + (task - panel * nrows);
-  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
-  const uint32_t voff = poff + lane * 16u;
-  const uint64_t pol = policy_evict_first(1.0f);
-
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
-  double2* my = reinterpret_cast<double2*>(smem + 128) + warp * (2 * 32 * CH);
-  if constexpr (kStep) {
-    if (lane == 0 && live) {
-      mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      mbar_arrive_expect_tx(bar, 2 * kPB);
-      bulk_g2s_hint(my, p.vin + static_cast<uint64_t>(r) * p.ldg_b + poff, kPB, bar, pol);
-      bulk_g2s_hint(my + 32 * CH, p.yin + static_cast<uint64_t>(r) * p.ldy_b + poff, kPB, bar, pol);
-    }
-  }
-  char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
-  const char* gb = p.g + voff;
-  double2 acc[CH];
-#pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    if constexpr (kSpmmAcc)
-      acc[c] = live ? *reinterpret_cast<const double2*>(ob + 512 * c) : make_double2(0.0, 0.0);
-    else
-      acc[c] = make_double2(0.0, 0.0);
-  }
-  const int64_t start = ld_rp<RP>(p.row_ptr, r);
-  const int cnt_all = live ? static_cast<int>(ld_rp<RP>(p.row_ptr, r + 1) - start) : 0;
-  for (int base = 0; base < cnt_all; base += 32) {
-    const int cnt = min(32, cnt_all - base);
-    int mc = 0;
-    Val mv{};
-    if (lane < cnt) {
-      mc = __ldg(p.col + start + base + lane);
-      mv = F::load(p.val, start + base + lane);
-    }
-    for (int k0 = 0; k0 < cnt; k0 += U) {
-      double2 w[U][CH];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int cidx = __shfl_sync(0xffffffffu, mc, (k0 + u) & 31);
-        if (k0 + u < cnt) {
-          const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
-#pragma unroll
-          for (int c = 0; c < CH; ++c) w[u][c] = __ldg(src + 32 * c);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        Val v;
-        if constexpr (std::is_same<Val, double>::value) {
-          v = __shfl_sync(0xffffffffu, mv, (k0 + u) & 31);
-        } else {
-          v.x = __shfl_sync(0xffffffffu, mv.x, (k0 + u) & 31);
-          v.y = __shfl_sync(0xffffffffu, mv.y, (k0 + u) & 31);
-        }
-        if (k0 + u < cnt) {
-#pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            double2 wv = w[u][c];
-            if constexpr (kFirst) wv = scale2(p.s2, wv);
-            acc[c] = F::mac(acc[c], v, wv);
-          }
-        }
-      }
-    }
-  }
-  if (!live) return;
-  if constexpr (kStep) mbar_wait(bar, 0);
-  const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
-  char* wb = kFirst ? p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff : nullptr;
-#pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    double2 own = make_double2(0.0, 0.0);
-    if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
-    double2 res;
-    if constexpr (kStep) {
-      const double2 vv = my[c * 32 + lane];
-      const double2 yy = my[32 * CH + c * 32 + lane];
-      res = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
-    } else if constexpr (kFirst) {
-      const double2 wn = scale2(p.s2, own);
-      st_hint(wb + 512 * c, wn, pol);
-      res = add2(scale2(p.s0, acc[c]), scale2(p.s1, wn));
-    } else if constexpr (kDeg1) {
-      res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own))));
-    } else {
-      res = acc[c];
-    }
-    st_hint(ob + 512 * c, res, pol);
-  }
-}
-
-template <class F, int CH, int U, class RP, int MINB>
-void launch_lean2(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
-  constexpr int kWarps = kThreads / 32;
-  k.n_panels = qv / (32 * CH);
-  const int64_t total = k.nrows * k.n_panels;
-  if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_lean2: too many tasks");
-  const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
-  const size_t smem = mode == StepMode::Step ? 128 + static_cast<size_t>(kWarps) * 2 * 32 * CH * 16 : 16;
-  auto run = [&](auto kern) {
-    if (smem > 48 * 1024)
-      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, kThreads, smem, ctx->stream>>>(k);
-  };
-  switch (mode) {
-    case StepMode::First: run(cheb_lean2_kernel<F, CH, U, 0, RP, MINB>); break;
-    case StepMode::Step: run(cheb_lean2_kernel<F, CH, U, 1, RP, MINB>); break;
-    case StepMode::Deg1: run(cheb_lean2_kernel<F, CH, U, 2, RP, MINB>); break;
-    case StepMode::Spmm: run(cheb_lean2_kernel<F, CH, U, 3, RP, MINB>); break;
-    case StepMode::SpmmAcc: run(cheb_lean2_kernel<F, CH, U, 4, RP, MINB>); break;
-  }
-  ADP_LAUNCH_CHECK();
-  ctx->launches += 1;
-}
-
-// ---- row-window kernel ----------------------------------------------------------------------
-// A CTA of WARPS warps owns WARPS consecutive rows (one per warp) of one column
-// panel. The gathered operand's rows [r0 - H, r0 + WARPS + H) -- the band every
-// row of the block touches through its near-diagonal entries (the x-line of a
-// stencil) and its own row -- are bulk-copied ONCE per CTA into shared memory;
-// gathers whose column falls in that window read shared memory, the rest read
-// global memory through L1 as in the lean kernel. Cuts the L2->SM gather
-// traffic of a 7-point stencil from 7 to 4 + (WARPS+2H)/WARPS row panels per row
-// and removes the own-row reload. Accumulation order per row is unchanged (CSR
-// order), so results are bitwise the lean kernel's.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-template <class F, int CH, int WARPS, int H, int MODE, class RP, int MINB>
-__global__ void __launch_bounds__(WARPS * 32, MINB) cheb_win_kernel(const LArgs p) {
-  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
-  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
-  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
-  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
-  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
-  constexpr uint32_t kPB = 32 * CH * 16u;
-  constexpr int kWin = WARPS + 2 * H;
-  using Val = typename F::Val;
-  extern __shared__ __align__(16) uint8_t smem[];  // [2 mbarriers | pad][window rows][warp][V, Y]
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int32_t nrows = static_cast<int32_t>(p.nrows);
-  const int32_t nblk = (nrows + WARPS - 1) / WARPS;
-  const int32_t panel = static_cast<int32_t>(blockIdx.x) / nblk;
-  const int32_t b = static_cast<int32_t>(blockIdx.x) - panel * nblk;
-  const int32_t rows = min(WARPS, nrows - b * WARPS);
-  const int64_t r0 = p.row_begin + static_cast<int64_t>(b) * WARPS;  // first out row of the block
-  const int64_t g0 = r0 + p.goff;                                     // its own row in the gathered operand
-  const int64_t wlo = g0 - H > 0 ? g0 - H : 0;
-  const int64_t whi = g0 + rows + H < p.g_rows ? g0 + rows + H : p.g_rows;
-  const uint32_t wn = static_cast<uint32_t>(whi - wlo);
-  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
-  const uint32_t voff = poff + lane * 16u;
-
-  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* vbar = wbar + 1;
-  double2* win = reinterpret_cast<double2*>(smem + 128);
-  double2* vy = win + kWin * 32 * CH;
-  if (threadIdx.x == 0) {
-    mbar_init(wbar, 1);
-    mbar_init(vbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    mbar_arrive_expect_tx(wbar, kPB * wn);
-    if constexpr (kStep) mbar_arrive_expect_tx(vbar, 2 * kPB * static_cast<uint32_t>(rows));
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const uint64_t pol = policy_evict_first(1.0f);
-    for (uint32_t i = lane; i < wn; i += 32)  // WARPS + 2H may exceed 32
-      bulk_g2s(win + i * 32 * CH, p.g + static_cast<uint64_t>(wlo + i) * p.ldg_b + poff, kPB, wbar);
-    if constexpr (kStep) {
-      if (lane < rows) {
-        bulk_g2s_hint(vy + lane * 2 * 32 * CH, p.vin + static_cast<uint64_t>(r0 + lane) * p.ldg_b + poff, kPB, vbar, pol);
-        bulk_g2s_hint(vy + lane * 2 * 32 * CH + 32 * CH, p.yin + static_cast<uint64_t>(r0 + lane) * p.ldy_b + poff, kPB,
-                      vbar, pol);
-      }
-    }
-  }
-  if (warp >= rows) return;
-  const uint64_t pol = policy_evict_first(1.0f);
-  const int64_t r = r0 + warp;
-  char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
-  const char* gb = p.g + voff;
-  double2 acc[CH];
-#pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    if constexpr (kSpmmAcc)
-      acc[c] = *reinterpret_cast<const double2*>(ob + 512 * c);
-    else
-      acc[c] = make_double2(0.0, 0.0);
-  }
-  bool ready = false;
-  const RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r));
-  const RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r + 1));
-  for (RP e = start; e < end; ++e) {
-    const int cidx = __ldg(p.col + e);
-    const Val v = F::load(p.val, static_cast<int64_t>(e));
-    const uint32_t rel = static_cast<uint32_t>(cidx - static_cast<int32_t>(wlo));
-    double2 w[CH];
-    if (rel < wn) {
-      if (!ready) {
-        mbar_wait(wbar, 0);
-        ready = true;
-      }
-#pragma unroll
-      for (int c = 0; c < CH; ++c) w[c] = win[rel * (32 * CH) + c * 32 + lane];
-    } else {
-      const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
-#pragma unroll
-      for (int c = 0; c < CH; ++c) w[c] = __ldg(src + 32 * c);
-    }
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      double2 wv = w[c];
-      if constexpr (kFirst) wv = scale2(p.s2, wv);
-      acc[c] = F::mac(acc[c], v, wv);
-    }
-  }
-  if (!ready) mbar_wait(wbar, 0);  // also: no CTA exit with bulk copies in flight
-  if constexpr (kStep) mbar_wait(vbar, 0);
-  const uint32_t own_rel = static_cast<uint32_t>(g0 + warp - wlo);
-  char* wb = kFirst ? p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff : nullptr;
-#pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    double2 own = make_double2(0.0, 0.0);
-    if constexpr (kNeedOwn) own = win[own_rel * (32 * CH) + c * 32 + lane];
-    double2 res;
-    if constexpr (kStep) {
-      const double2 vv = vy[warp * 2 * 32 * CH + c * 32 + lane];
-      const double2 yy = vy[warp * 2 * 32 * CH + 32 * CH + c * 32 + lane];
-      res = add2(sub2(add2(scale2(p.s0, acc[c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
-    } else if constexpr (kFirst) {
-      const double2 wn2 = scale2(p.s2, own);
-      st_hint(wb + 512 * c, wn2, pol);
-      res = add2(scale2(p.s0, acc[c]), scale2(p.s1, wn2));
-    } else if constexpr (kDeg1) {
-      res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[c]), scale2(p.s3, own))));
-    } else {
-      res = acc[c];
-    }
-    st_hint(ob + 512 * c, res, pol);
-  }
-}
-
-template <class F, int CH, int WARPS, int H, class RP, int MINB>
-void launch_win(adp_ctx* ctx, StepMode mode, LArgs k, int64_t qv) {
-  k.n_panels = qv / (32 * CH);
-  const int64_t nblk = (k.nrows + WARPS - 1) / WARPS;
-  const int64_t total = nblk * k.n_panels;
-  if (total >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_win: too many blocks");
-  constexpr size_t kWinBytes = static_cast<size_t>(WARPS + 2 * H) * 32 * CH * 16;
-  const size_t smem = 128 + kWinBytes + (mode == StepMode::Step ? static_cast<size_t>(WARPS) * 2 * 32 * CH * 16 : 0);
-  auto run = [&](auto kern) {
-    if (smem > 48 * 1024)
-      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<static_cast<int>(total), WARPS * 32, smem, ctx->stream>>>(k);
-  };
-  switch (mode) {
-    case StepMode::First: run(cheb_win_kernel<F, CH, WARPS, H, 0, RP, MINB>); break;
-    case StepMode::Step: run(cheb_win_kernel<F, CH, WARPS, H, 1, RP, MINB>); break;
-    case StepMode::Deg1: run(cheb_win_kernel<F, CH, WARPS, H, 2, RP, MINB>); break;
-    case StepMode::Spmm: run(cheb_win_kernel<F, CH, WARPS, H, 3, RP, MINB>); break;
-    case StepMode::SpmmAcc: run(cheb_win_kernel<F, CH, WARPS, H, 4, RP, MINB>); break;
-  }
-  ADP_LAUNCH_CHECK();
-  ctx->launches += 1;
-}
-
-// ---- column-segment kernel (MaSpMM row blocks) ------------------------------------------
-// A warp owns an R-row block of one panel and walks the block's precomputed
-// distinct columns (segments.cpp): each W row panel is loaded ONCE and applied,
-// from registers, to every row of the block whose bit is set in the segment's
-// mask. Unlike the union kernel the walk has no loop-carried dependency (the
-// segment list is data), so U segments are loaded ahead. Per row the products
-// still accumulate in ascending column order: bitwise the reference's.
-struct SArgs {
-  LArgs l;
-  const int64_t* blk_ptr;
-  const int32_t* seg_col;
-  const uint32_t* seg_mask;
-  const void* seg_val;
-};
-
-template <class F, int CH, int R, int U, int MODE, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) cheb_seg_kernel(const SArgs sa) {
-  constexpr bool kStep = MODE == static_cast<int>(StepMode::Step);
-  constexpr bool kFirst = MODE == static_cast<int>(StepMode::First);
-  constexpr bool kDeg1 = MODE == static_cast<int>(StepMode::Deg1);
-  constexpr bool kSpmmAcc = MODE == static_cast<int>(StepMode::SpmmAcc);
-  constexpr bool kNeedOwn = kStep || kFirst || kDeg1;
-  constexpr int kWarps = kThreads / 32;
-  constexpr uint32_t kPB = 32 * CH * 16u;
-  using Val = typename F::Val;
-  const LArgs& p = sa.l;
-  extern __shared__ __align__(16) uint8_t smem[];  // [8 mbarriers][warp][row][V, Y] panels
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int32_t nrows = static_cast<int32_t>(p.nrows);
-  const int32_t nblk = (nrows + R - 1) / R;
-  const int32_t task = static_cast<int32_t>(blockIdx.x) * kWarps + warp;
-  if (task >= nblk * static_cast<int32_t>(p.n_panels)) return;
-  const int32_t panel = task / nblk;
-  const int32_t b = task - panel * nblk;
-  const int64_t r0 = static_cast<int64_t>(b) * R;  // segments cover the whole operator (row_begin == 0)
-  const int rows = min(R, nrows - b * R);
-  const uint32_t poff = static_cast<uint32_t>(panel) * kPB;
-  const uint32_t voff = poff + lane * 16u;
-  const uint64_t pol = policy_evict_first(1.0f);
-
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
-  double2* my = reinterpret_cast<double2*>(smem + 128) + warp * (R * 2 * 32 * CH);
-  if constexpr (kStep) {
-    if (lane == 0) {
-      mbar_init(bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      mbar_arrive_expect_tx(bar, 2 * kPB * rows);
-    }
-    __syncwarp();
-    if (lane < rows) {
-      bulk_g2s_hint(my + lane * (2 * 32 * CH), p.vin + static_cast<uint64_t>(r0 + lane) * p.ldg_b + poff, kPB, bar, pol);
-      bulk_g2s_hint(my + lane * (2 * 32 * CH) + 32 * CH, p.yin + static_cast<uint64_t>(r0 + lane) * p.ldy_b + poff, kPB,
-                    bar, pol);
-    }
-  }
-  const char* gb = p.g + voff;
-  double2 acc[R][CH];
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      if constexpr (kSpmmAcc)
-        acc[i][c] = i < rows ? *reinterpret_cast<const double2*>(p.out + static_cast<uint64_t>(r0 + i) * p.ldo_b + voff + 512 * c)
-                             : make_double2(0.0, 0.0);
-      else
-        acc[i][c] = make_double2(0.0, 0.0);
-    }
-  const int64_t s0 = __ldg(sa.blk_ptr + b), s1 = __ldg(sa.blk_ptr + b + 1);
-  for (int64_t s = s0; s < s1; s += U) {
-    int col[U];
-    uint32_t msk[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      col[u] = 0;
-      msk[u] = 0;
-      if (s + u < s1) {
-        col[u] = __ldg(sa.seg_col + s + u);
-        msk[u] = __ldg(sa.seg_mask + s + u);
-      }
-    }
-    double2 w[U][CH];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (s + u < s1) {
-        const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(col[u])) * p.ldg_b);
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          w[u][c] = __ldg(src + 32 * c);
-          if constexpr (kFirst) w[u][c] = scale2(p.s2, w[u][c]);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        if ((msk[u] >> i) & 1u) {
-          const Val v = F::load(sa.seg_val, (s + u) * R + i);
-#pragma unroll
-          for (int c = 0; c < CH; ++c) acc[i][c] = F::mac(acc[i][c], v, w[u][c]);
-        }
-      }
-    }
-  }
-  if constexpr (kStep) {
-    __syncwarp();
-    mbar_wait(bar, 0);
-  }
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    if (i >= rows) break;
-    const int64_t r = r0 + i;
-    const double2* own_src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(r + p.goff) * p.ldg_b);
-    char* ob = p.out + static_cast<uint64_t>(r) * p.ldo_b + voff;
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      double2 own = make_double2(0.0, 0.0);
-      if constexpr (kNeedOwn) own = __ldg(own_src + 32 * c);
-      double2 res;
-      if constexpr (kStep) {
-        const double2 vv = my[i * (2 * 32 * CH) + c * 32 + lane];
-        const double2 yy = my[i * (2 * 32 * CH) + 32 * CH + c * 32 + lane];
-        res = add2(sub2(add2(scale2(p.s0, acc[i][c]), scale2(p.s1, own)), vv), scale2(p.s2, yy));
-      } else if constexpr (kFirst) {
-        const double2 wn = scale2(p.s2, own);
-        st_hint(p.wout + static_cast<uint64_t>(r) * p.ldo_b + voff + 512 * c, wn, pol);
-        res = add2(scale2(p.s0, acc[i][c]), scale2(p.s1, wn));
-      } else if constexpr (kDeg1) {
-        res = add2(scale2(p.s0, own), scale2(p.s1, add2(scale2(p.s2, acc[i][c]), scale2(p.s3, own))));
-      } else {
-        res = acc[i][c];
-      }
-      st_hint(ob + 512 * c, res, pol);
-    }
-  }
-}
-
-template <class F, int CH, int R, int U, int MINB>
-bool launch_seg(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, const adp_csr* a) {
-  if (k.row_begin != 0 || k.nrows != a->n_rows) return false;  // segments cover whole operators
-  const Segments* sg = get_segments(const_cast<adp_csr*>(a), R);
-  constexpr int kWarps = kThreads / 32;
-  SArgs sa{};
-  sa.l = k;
-  sa.l.n_panels = qv / (32 * CH);
-  sa.blk_ptr = static_cast<const int64_t*>(sg->d_blk_ptr);
-  sa.seg_col = static_cast<const int32_t*>(sg->d_col);
-  sa.seg_mask = static_cast<const uint32_t*>(sg->d_mask);
-  sa.seg_val = sg->d_val;
-  const int64_t total = sg->n_blocks * sa.l.n_panels;
-  if (total >= (int64_t{1} << 31)) return false;
-  const int grid = static_cast<int>((total + kWarps - 1) / kWarps);
-  const size_t smem = mode == StepMode::Step ? 128 + static_cast<size_t>(kWarps) * R * 2 * 32 * CH * 16 : 16;
-  auto run = [&](auto kern) {
-    if (smem > 48 * 1024)
-      ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, kThreads, smem, ctx->stream>>>(sa);
-  };
-  switch (mode) {
-    case StepMode::First: run(cheb_seg_kernel<F, CH, R, U, 0, MINB>); break;
-    case StepMode::Step: run(cheb_seg_kernel<F, CH, R, U, 1, MINB>); break;
-    case StepMode::Deg1: run(cheb_seg_kernel<F, CH, R, U, 2, MINB>); break;
-    case StepMode::Spmm: run(cheb_seg_kernel<F, CH, R, U, 3, MINB>); break;
-    case StepMode::SpmmAcc: run(cheb_seg_kernel<F, CH, R, U, 4, MINB>); break;
-  }
-  ADP_LAUNCH_CHECK();
-  ctx->launches += 1;
-  return true;
-}
-
 // Full-panel launch for qv vectors (qv a multiple of the chosen panel). Geometry
 // measured on configs 1-2 (tools/tune_step.py): widest panel with one gathered
 // row in flight per group and many resident warps.
 template <class F, class RP>
 void launch_full(adp_ctx* ctx, StepMode mode, const LArgs& k, int64_t qv, int64_t cap, const adp_csr* a) {
-  switch (ctx->variant) {  // row-block union kernel (tuning variants 21-24)
-    case 21: if (qv % 64 == 0) return launch_union<F, 2, 4, RP, 3>(ctx, mode, k, qv); break;
-    case 22: if (qv % 128 == 0) return launch_union<F, 4, 2, RP, 2>(ctx, mode, k, qv); break;
-    case 23: if (qv % 64 == 0) return launch_union<F, 2, 2, RP, 4>(ctx, mode, k, qv); break;
-    case 24: if (qv % 32 == 0) return launch_union<F, 1, 4, RP, 4>(ctx, mode, k, qv); break;
-    // deeper gather batches for long rows (tuning variants 31-33)
-    case 31: if (qv % 32 == 0) return launch_lean<F, 32, 1, 8, RP, 4>(ctx, mode, k, qv); break;
-    case 32: if (qv % 64 == 0) return launch_lean<F, 32, 2, 4, RP, 3>(ctx, mode, k, qv); break;
-    case 33: if (qv % 128 == 0) return launch_lean<F, 32, 4, 4, RP, 2>(ctx, mode, k, qv); break;
-    // column-segment (MaSpMM row-block) kernel (tuning variants 41-46)
-    case 41: if (qv % 64 == 0 && launch_seg<F, 2, 4, 2, 2>(ctx, mode, k, qv, a)) return; break;
-    case 42: if (qv % 128 == 0 && launch_seg<F, 4, 2, 2, 2>(ctx, mode, k, qv, a)) return; break;
-    case 43: if (qv % 32 == 0 && launch_seg<F, 1, 8, 2, 2>(ctx, mode, k, qv, a)) return; break;
-    case 44: if (qv % 64 == 0 && launch_seg<F, 2, 2, 4, 3>(ctx, mode, k, qv, a)) return; break;
-    case 45: if (qv % 32 == 0 && launch_seg<F, 1, 4, 4, 4>(ctx, mode, k, qv, a)) return; break;
-    case 46: if (qv % 128 == 0 && launch_seg<F, 4, 4, 1, 1>(ctx, mode, k, qv, a)) return; break;
-    case 47: if (qv % 128 == 0 && launch_seg<F, 4, 4, 1, 2>(ctx, mode, k, qv, a)) return; break;
-    case 48: if (qv % 64 == 0 && launch_seg<F, 2, 4, 2, 3>(ctx, mode, k, qv, a)) return; break;
-    case 49: if (qv % 64 == 0 && launch_seg<F, 2, 4, 1, 4>(ctx, mode, k, qv, a)) return; break;
-    case 40: if (qv % 128 == 0 && launch_seg<F, 4, 3, 1, 2>(ctx, mode, k, qv, a)) return; break;
-    // lane-parallel metadata (tuning variants 51-56)
-    case 51: if (qv % 128 == 0) return launch_lean2<F, 4, 2, RP, 2>(ctx, mode, k, qv); break;
-    case 52: if (qv % 128 == 0) return launch_lean2<F, 4, 4, RP, 2>(ctx, mode, k, qv); break;
-    case 53: if (qv % 64 == 0) return launch_lean2<F, 2, 4, RP, 3>(ctx, mode, k, qv); break;
-    case 54: if (qv % 64 == 0) return launch_lean2<F, 2, 8, RP, 2>(ctx, mode, k, qv); break;
-    case 55: if (qv % 32 == 0) return launch_lean2<F, 1, 8, RP, 4>(ctx, mode, k, qv); break;
-    case 56: if (qv % 128 == 0) return launch_lean2<F, 4, 1, RP, 4>(ctx, mode, k, qv); break;
-    // row-window kernel (tuning variants 61-66)
-    case 61: if (qv % 128 == 0) return launch_win<F, 4, 8, 1, RP, 4>(ctx, mode, k, qv); break;
-    case 62: if (qv % 128 == 0) return launch_win<F, 4, 16, 1, RP, 2>(ctx, mode, k, qv); break;
-    case 63: if (qv % 64 == 0) return launch_win<F, 2, 8, 1, RP, 6>(ctx, mode, k, qv); break;
-    case 64: if (qv % 128 == 0) return launch_win<F, 4, 32, 1, RP, 1>(ctx, mode, k, qv); break;
-    case 65: if (qv % 64 == 0) return launch_win<F, 2, 16, 1, RP, 3>(ctx, mode, k, qv); break;
-    case 66: if (qv % 128 == 0) return launch_win<F, 4, 4, 1, RP, 8>(ctx, mode, k, qv); break;
-    // multi-row lean kernel (tuning variants 101-108)
-    case 101: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 2, true, RP, 4>(ctx, mode, k, qv); break;
-    case 102: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 4, true, RP, 4>(ctx, mode, k, qv); break;
-    case 103: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 8, true, RP, 4>(ctx, mode, k, qv); break;
-    case 104: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 2, false, RP, 4>(ctx, mode, k, qv); break;
-    case 105: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 4, false, RP, 4>(ctx, mode, k, qv); break;
-    case 106: if (qv % 128 == 0) return launch_leanm<F, 32, 4, 8, false, RP, 4>(ctx, mode, k, qv); break;
-    case 107: if (qv % 64 == 0) return launch_leanm<F, 32, 2, 4, true, RP, 6>(ctx, mode, k, qv); break;
-    case 108: if (qv % 64 == 0) return launch_leanm<F, 32, 2, 4, false, RP, 6>(ctx, mode, k, qv); break;
-    default: break;
-  }
   if (qv % 128 == 0 && cap >= 128) return launch_lean<F, 32, 4, 1, RP, 4>(ctx, mode, k, qv);
   if (qv % 64 == 0 && cap >= 64) return launch_lean<F, 32, 2, 1, RP, 6>(ctx, mode, k, qv);
   if (qv % 32 == 0 && cap >= 32) return launch_lean<F, 32, 1, 1, RP, 8>(ctx, mode, k, qv);

@@ -197,7 +197,6 @@ struct LnArgs {
   const int4* runs;
   const int32_t* prefix;   // band plans: entries before each row's core (nullptr: no band block)
   const int32_t* pat_len;  // band plans: core entries of each pattern
-  uint32_t* sched;  // pipelined kernel: [0] next task ticket, [1] finished warps (both 0 between launches)
   double s0, s1, s2, s3;
 };
 
@@ -525,228 +524,6 @@ bool launch_line_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv,
   return true;
 }
 
-// ---- pipelined variant (Step mode) -----------------------------------------------------
-// Same work split and arithmetic as cheb_line_kernel, but every gathered row
-// panel travels by TMA bulk copy into a per-warp ring of S shared-memory stages
-// (one mbarrier each), so a warp keeps up to S items in flight without holding
-// them in registers -- the line kernel on config 4 is bound by the latency of
-// its register-staged gathers (profiles/). Items of a task (row block, panel):
-// one per column run (its R + m - 1 rows), then [own rows of W, V rows], then
-// [Y rows]. The grid is persistent and claims tasks in order from a global
-// ticket (two at a time), so the warps advance as one compact wavefront -- the
-// order of the one-task-per-warp kernels, which keeps the gathered operand's
-// stencil reuse in L2 (a static round-robin split drifts apart and loses it:
-// 152 GB of DRAM reads per config-4 step instead of 63). Lane 0 issues the
-// copies of item s + S as soon as item s is consumed, across task boundaries;
-// the tasks between producer and consumer wait in a per-warp queue.
-struct Cursor {
-  int32_t task, item, nrun, run0, rows;
-};
-
-template <int R, int SR, class RP>
-__device__ __forceinline__ void cursor_load(Cursor& c, const LnArgs& p, int32_t task) {
-  c.task = task;
-  c.item = 0;
-  c.nrun = 0;
-  c.run0 = 0;
-  c.rows = 0;
-  if (task >= p.nblk * p.n_panels) return;
-  const int32_t panel = task / p.nblk;
-  const int32_t b = task - panel * p.nblk;
-  c.rows = min(R, p.nrows - b * R);
-  const int32_t pid = __ldg(p.blk_pat + b);
-  if (pid >= 0) {
-    c.run0 = __ldg(p.pat_ptr + pid);
-    c.nrun = __ldg(p.pat_ptr + pid + 1) - c.run0;
-  }
-}
-
-template <class F, int CH, int R, int MM, int S, int NW, class RP, int MINB>
-__global__ void __launch_bounds__(NW * 32, MINB)
-    cheb_linep_kernel(const LnArgs p, int32_t total_warps, const __grid_constant__ CUtensorMap tm_run,
-                      const __grid_constant__ CUtensorMap tm_own, const __grid_constant__ CUtensorMap tm_v,
-                      const __grid_constant__ CUtensorMap tm_y) {
-  constexpr uint32_t kPB = 32 * CH * 16u;
-  constexpr int kW = R + MM - 1;
-  constexpr int SR = kW > 2 * R ? kW : 2 * R;  // rows per stage
-  using Val = typename F::Val;
-  extern __shared__ __align__(16) uint8_t smem[];  // [NW][S mbarriers] | [NW][S][SR row panels]
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * S;
-  double2* ring = reinterpret_cast<double2*>(smem + ((NW * S * 8 + 127) / 128) * 128) + warp * (S * SR * 32 * CH);
-  __shared__ int32_t tq[NW][8];
-  const int32_t ntask = p.nblk * p.n_panels;
-  if (lane == 0)
-    for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  __syncwarp();
-  const uint64_t pol = policy_evict_first(1.0f);
-
-  // producer: one 2-D TMA tile copy per item (two for [own, V]) into stage s
-  constexpr int32_t kPE = static_cast<int32_t>(kPB / 8);  // panel width in fp64 words
-  auto issue = [&](const Cursor& c, int s) {
-    if (lane == 0) {
-      const int32_t panel = c.task / p.nblk;
-      const int32_t r0 = (c.task - panel * p.nblk) * R;
-      const int32_t x = panel * kPE;
-      double2* dst = ring + s * (SR * 32 * CH);
-      if (c.item < c.nrun) {  // run: gathered rows c0 .. c0 + kW - 1 (the last MM - m unused)
-        const int4 rn = __ldg(p.runs + c.run0 + c.item);
-        mbar_arrive_expect_tx(bars + s, kW * kPB);
-        tma2d(dst, &tm_run, x, r0 + rn.x, bars + s);
-      } else if (c.item == c.nrun) {  // own rows of W, then V rows
-        mbar_arrive_expect_tx(bars + s, 2 * R * kPB);
-        tma2d(dst, &tm_own, x, static_cast<int32_t>(r0 + p.goff), bars + s);
-        tma2d_hint(dst + R * 32 * CH, &tm_v, x, r0, bars + s, pol);
-      } else {  // Y rows
-        mbar_arrive_expect_tx(bars + s, R * kPB);
-        tma2d_hint(dst, &tm_y, x, r0, bars + s, pol);
-      }
-    }
-    __syncwarp();
-  };
-  constexpr int32_t kBatch = 2;
-  int32_t bnext = 0, bleft = 0;
-  auto claim = [&]() -> int32_t {
-    if (bleft == 0) {
-      if (bnext >= ntask && bnext > 0) return ntask;
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(p.sched, static_cast<uint32_t>(kBatch));
-      bnext = static_cast<int32_t>(__shfl_sync(0xffffffffu, base, 0));
-      bleft = kBatch;
-    }
-    if (bnext >= ntask) return ntask;
-    --bleft;
-    return bnext++;
-  };
-  int32_t ptseq = 0, ctseq = 0;
-  auto advance_p = [&](Cursor& c) {
-    if (++c.item == c.nrun + 2) {
-      const int32_t t = claim();
-      ++ptseq;
-      if (lane == 0) tq[warp][ptseq & 7] = t;
-      __syncwarp();
-      cursor_load<R, SR, RP>(c, p, t);
-    }
-  };
-  auto advance_c = [&](Cursor& c) {
-    if (++c.item == c.nrun + 2) {
-      ++ctseq;
-      cursor_load<R, SR, RP>(c, p, tq[warp][ctseq & 7]);
-    }
-  };
-
-  Cursor pc, cc;
-  {
-    const int32_t t = claim();
-    if (lane == 0) tq[warp][0] = t;
-    __syncwarp();
-    cursor_load<R, SR, RP>(pc, p, t);
-  }
-  cc = pc;
-  int32_t pseq = 0;
-  for (; pseq < S && pc.task < ntask; ++pseq) {
-    issue(pc, pseq);
-    advance_p(pc);
-  }
-  int32_t cseq = 0;
-  double2 acc[R][CH];
-  int64_t rs[R];
-  while (cc.task < ntask) {
-    const int32_t panel = cc.task / p.nblk;
-    const int32_t r0 = (cc.task - panel * p.nblk) * R;
-    const uint32_t voff = static_cast<uint32_t>(panel) * kPB + lane * 16u;
-    if (cc.item == 0) {
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-#pragma unroll
-        for (int c = 0; c < CH; ++c) acc[i][c] = make_double2(0.0, 0.0);
-      if (cc.nrun > 0) {
-#pragma unroll
-        for (int i = 0; i < R; ++i) rs[i] = ld_rp<RP>(p.row_ptr, r0 + i);
-      } else {  // row by row from global memory, CSR order
-        const char* gb = p.g + voff;
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-          if (i < cc.rows) {
-            const RP start = static_cast<RP>(ld_rp<RP>(p.row_ptr, r0 + i));
-            const RP end = static_cast<RP>(ld_rp<RP>(p.row_ptr, r0 + i + 1));
-            for (RP e = start; e < end; ++e) {
-              const int cidx = __ldg(p.col + e);
-              const Val v = F::load(p.val, static_cast<int64_t>(e));
-              const double2* src = reinterpret_cast<const double2*>(gb + static_cast<uint64_t>(static_cast<uint32_t>(cidx)) * p.ldg_b);
-#pragma unroll
-              for (int c = 0; c < CH; ++c) acc[i][c] = F::mac(acc[i][c], v, __ldg(src + 32 * c));
-            }
-          }
-        }
-      }
-    }
-    const int s = cseq % S;
-    mbar_wait(bars + s, static_cast<uint32_t>(cseq / S) & 1u);
-    const double2* st = ring + s * (SR * 32 * CH);
-    if (cc.item < cc.nrun) {
-      const int4 rn = __ldg(p.runs + cc.run0 + cc.item);
-      const int m = rn.z;
-      double2 w[kW][CH];
-#pragma unroll
-      for (int j = 0; j < kW; ++j)
-        if (j < R + m - 1)
-#pragma unroll
-          for (int c = 0; c < CH; ++c) w[j][c] = st[j * (32 * CH) + c * 32 + lane];
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-#pragma unroll
-        for (int t = 0; t < MM; ++t) {
-          if (t < m) {
-            const Val v = F::load(p.val, rs[i] + rn.y + t);
-#pragma unroll
-            for (int c = 0; c < CH; ++c) acc[i][c] = F::mac(acc[i][c], v, w[i + t][c]);
-          }
-        }
-      }
-    } else if (cc.item == cc.nrun) {
-      // partial = ((s0 * aw) + (s1 * w)) - v   (cheb_filter.cpp:170-171, 176-177)
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-        if (i < cc.rows)
-#pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            const double2 own = st[i * (32 * CH) + c * 32 + lane];
-            const double2 vv = st[(R + i) * (32 * CH) + c * 32 + lane];
-            acc[i][c] = sub2(add2(scale2(p.s0, acc[i][c]), scale2(p.s1, own)), vv);
-          }
-    } else {
-      // v = partial + (s2 * y)
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-        if (i < cc.rows) {
-          char* ob = p.out + static_cast<uint64_t>(r0 + i) * p.ldo_b + voff;
-#pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            const double2 yy = st[i * (32 * CH) + c * 32 + lane];
-            st_hint(ob + 512 * c, add2(acc[i][c], scale2(p.s2, yy)), pol);
-          }
-        }
-    }
-    __syncwarp();  // stage s consumed by every lane: refill it
-    if (pc.task < ntask) {
-      issue(pc, s);
-      advance_p(pc);
-      ++pseq;
-    }
-    ++cseq;
-    advance_c(cc);
-  }
-  if (lane == 0) {  // the last warp out re-arms the ticket for the next launch
-    const uint32_t prev = atomicAdd(p.sched + 1, 1u);
-    if (prev == static_cast<uint32_t>(total_warps) - 1) {
-      p.sched[0] = 0;
-      p.sched[1] = 0;
-    }
-  }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -776,88 +553,10 @@ CUtensorMap make_map(const void* base, int64_t rows, int64_t width, int64_t ld_b
   return m;
 }
 
-template <class F, int CH, int R, int MM, int S, int NW, class RP, int MINB>
-bool launch_linep_cfg(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
-  if (mode != StepMode::Step) return launch_line_cfg<F, CH, R, MM, RP, 2>(ctx, mode, s, qv, 0.0);
-  const adp_csr* a = s.a;
-  if (qv % (32 * CH) != 0) return false;
-  const LinePlan* plan = get_line_plan(const_cast<adp_csr*>(a), R, MM);
-  const int epv = a->dtype == ADP_C128 ? 1 : 2;
-  LnArgs k{};
-  k.row_ptr = a->row_ptr;
-  k.col = a->col_idx;
-  k.val = a->values;
-  k.g = static_cast<const char*>(s.gsrc);
-  k.vin = static_cast<const char*>(s.vin);
-  k.yin = static_cast<const char*>(s.yin);
-  k.out = static_cast<char*>(s.out);
-  k.ldg_b = static_cast<uint32_t>((s.ld / epv) * 16);
-  k.ldy_b = static_cast<uint32_t>((s.ld_y / epv) * 16);
-  k.ldo_b = static_cast<uint32_t>((s.ld_out / epv) * 16);
-  k.nrows = static_cast<int32_t>(a->n_rows);
-  k.nblk = static_cast<int32_t>(plan->n_blocks);
-  k.n_panels = static_cast<int32_t>(qv / (32 * CH));
-  k.goff = s.goff;
-  k.blk_pat = static_cast<const int32_t*>(plan->d_blk_pat);
-  k.pat_ptr = static_cast<const int32_t*>(plan->d_pat_ptr);
-  k.runs = static_cast<const int4*>(plan->d_runs);
-  k.sched = static_cast<uint32_t*>(ctx->sched.get(16));
-  if (!ctx->sched_ready) {
-    ADP_CUDA(cudaMemsetAsync(k.sched, 0, 16, ctx->stream));
-    ctx->sched_ready = true;
-  }
-  k.s0 = s.s0;
-  k.s1 = s.s1;
-  k.s2 = s.s2;
-  const int64_t total = plan->n_blocks * k.n_panels;
-  if (total >= (int64_t{1} << 31)) return false;
-  constexpr int kW = R + MM - 1;
-  constexpr int SR = kW > 2 * R ? kW : 2 * R;
-  const size_t smem = ((NW * S * 8 + 127) / 128) * 128 + static_cast<size_t>(NW) * S * SR * 32 * CH * 16;
-  auto kern = cheb_linep_kernel<F, CH, R, MM, S, NW, RP, MINB>;
-  if (smem > 48 * 1024)
-    ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  int per_sm = 0;
-  ADP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem));
-  if (per_sm < 1) return false;
-  const int64_t warps = std::min<int64_t>(static_cast<int64_t>(per_sm) * ctx->sm_count * NW, total);
-  const int grid = static_cast<int>((warps + NW - 1) / NW);
-  const int64_t width = qv * 2;  // fp64 words per row
-  constexpr int kPE = 32 * CH * 2;
-  const CUtensorMap tm_run = make_map(s.gsrc, a->n_cols, width, k.ldg_b, kW, kPE);
-  const CUtensorMap tm_own = make_map(s.gsrc, a->n_cols, width, k.ldg_b, R, kPE);
-  const CUtensorMap tm_v = make_map(s.vin, a->n_rows, width, k.ldg_b, R, kPE);
-  const CUtensorMap tm_y = make_map(s.yin, a->n_rows, width, k.ldy_b, R, kPE);
-  kern<<<grid, NW * 32, smem, ctx->stream>>>(k, grid * NW, tm_run, tm_own, tm_v, tm_y);
-  ADP_LAUNCH_CHECK();
-  ctx->launches += 1;
-  return true;
-}
-
 template <class F, class RP>
 bool dispatch_line(adp_ctx* ctx, StepMode mode, const StepArgs& s, int64_t qv) {
-  switch (ctx->variant) {
-    case 81: return launch_line_cfg<F, 2, 4, 3, RP, 2>(ctx, mode, s, qv, 0.0);
-    case 82: return launch_line_cfg<F, 4, 2, 3, RP, 2>(ctx, mode, s, qv, 0.0);
-    case 83: return launch_line_cfg<F, 1, 8, 3, RP, 2>(ctx, mode, s, qv, 0.0);
-    case 84: return launch_line_cfg<F, 2, 4, 4, RP, 2>(ctx, mode, s, qv, 0.0);
-    case 85: return launch_line_cfg<F, 1, 8, 4, RP, 2>(ctx, mode, s, qv, 0.0);
-    case 86: return launch_line_cfg<F, 2, 2, 3, RP, 3>(ctx, mode, s, qv, 0.0);
-    case 87: return launch_line_cfg<F, 1, 4, 3, RP, 3>(ctx, mode, s, qv, 0.0);
-    case 88: return launch_line_cfg<F, 2, 2, 3, RP, 2, 2>(ctx, mode, s, qv, 0.0);
-    case 89: return launch_line_cfg<F, 2, 4, 3, RP, 1, 2>(ctx, mode, s, qv, 0.0);
-    case 90: return launch_line_cfg<F, 1, 4, 3, RP, 2, 2>(ctx, mode, s, qv, 0.0);
-    case 91: return launch_line_cfg<F, 2, 2, 3, RP, 4, 1>(ctx, mode, s, qv, 0.0);
-    case 98: return launch_line_cfg<F, 2, 3, 3, RP, 2, 1>(ctx, mode, s, qv, 0.0);
-    // pipelined (TMA ring) variants: <CH, R, MM, S, NW, MINB>
-    case 92: return launch_linep_cfg<F, 2, 2, 3, 6, 4, RP, 1>(ctx, mode, s, qv);
-    case 93: return launch_linep_cfg<F, 2, 4, 3, 3, 4, RP, 1>(ctx, mode, s, qv);
-    case 94: return launch_linep_cfg<F, 4, 2, 3, 3, 4, RP, 1>(ctx, mode, s, qv);
-    case 95: return launch_linep_cfg<F, 2, 2, 3, 4, 4, RP, 1>(ctx, mode, s, qv);
-    case 96: return launch_linep_cfg<F, 1, 4, 3, 4, 4, RP, 1>(ctx, mode, s, qv);
-    case 97: return launch_linep_cfg<F, 2, 4, 3, 2, 4, RP, 1>(ctx, mode, s, qv);
-    default: return false;
-  }
+  // variant 3: the line kernel forced (its automatic geometry: R = 2 rows, runs <= 3, 1 KB panels)
+  return ctx->variant == 3 && launch_line_cfg<F, 2, 2, 3, RP, 3>(ctx, mode, s, qv, 0.0);
 }
 
 }  // namespace

@@ -330,49 +330,18 @@ void dispatch(adp_ctx* ctx, StepMode mode, KArgs k) {
     launch_mode<F, 16, 1, 8, RP, 2, true>(ctx, mode, k, k.nrows);
     return;
   }
-  // Tuning variants (adp_ctx_set_tuning); 0 = default.
-  int variant = ctx->variant;
-  if (ctx->panel_cols > 0) {  // explicit panel width: closest chunk count
-    const int epv = std::is_same<F, RealF>::value ? 2 : 1;
-    const int64_t ch = std::max<int64_t>(1, std::min<int64_t>(4, ctx->panel_cols / epv / 32));
-    variant = ch == 1 ? 4 : (ch == 2 ? 2 : 1);
-  }
   auto go = [&](int64_t ch, auto launcher) {
     k.n_panels = panels_for(qv, ch);
     launcher(k.nrows * k.n_panels);
   };
-  switch (variant) {
-    case 1:  // 4 chunks (2 KB fp64 panels), evict-first streaming
-      go(4, [&](int64_t t) { launch_mode<F, 32, 4, 4, RP, 2, true>(ctx, mode, k, t); });
-      break;
-    case 2:  // 2 chunks (1 KB panels), 3 blocks / SM
-      go(2, [&](int64_t t) { launch_mode<F, 32, 2, 4, RP, 3, true>(ctx, mode, k, t); });
-      break;
-    case 3:  // 2 chunks, 8 rows in flight
-      go(2, [&](int64_t t) { launch_mode<F, 32, 2, 8, RP, 2, true>(ctx, mode, k, t); });
-      break;
-    case 4:  // 1 chunk (512 B panels), 3 blocks / SM
-      go(1, [&](int64_t t) { launch_mode<F, 32, 1, 8, RP, 3, true>(ctx, mode, k, t); });
-      break;
-    case 5:  // 1 chunk, 4 blocks / SM
-      go(1, [&](int64_t t) { launch_mode<F, 32, 1, 8, RP, 4, true>(ctx, mode, k, t); });
-      break;
-    case 6:  // 2 chunks, 4 blocks / SM
-      go(2, [&](int64_t t) { launch_mode<F, 32, 2, 4, RP, 4, true>(ctx, mode, k, t); });
-      break;
-    case 7:  // 4 chunks, no cache hints (round-1 baseline)
-      go(4, [&](int64_t t) { launch_mode<F, 32, 4, 4, RP, 2, false>(ctx, mode, k, t); });
-      break;
-    default: {  // automatic: <= 4 chunks per panel, balanced across panels
-      const int64_t n_panels = (qv + 127) / 128;
-      const int64_t ch = (((qv + n_panels - 1) / n_panels) + 31) / 32;
-      switch (ch) {
-        case 1: go(1, [&](int64_t t) { launch_mode<F, 32, 1, 8, RP, 3, true>(ctx, mode, k, t); }); break;
-        case 2: go(2, [&](int64_t t) { launch_mode<F, 32, 2, 4, RP, 3, true>(ctx, mode, k, t); }); break;
-        case 3: go(3, [&](int64_t t) { launch_mode<F, 32, 3, 4, RP, 2, true>(ctx, mode, k, t); }); break;
-        default: go(4, [&](int64_t t) { launch_mode<F, 32, 4, 4, RP, 2, true>(ctx, mode, k, t); }); break;
-      }
-    }
+  // <= 4 chunks per panel, balanced across panels
+  const int64_t n_panels = (qv + 127) / 128;
+  const int64_t ch = (((qv + n_panels - 1) / n_panels) + 31) / 32;
+  switch (ch) {
+    case 1: go(1, [&](int64_t t) { launch_mode<F, 32, 1, 8, RP, 3, true>(ctx, mode, k, t); }); break;
+    case 2: go(2, [&](int64_t t) { launch_mode<F, 32, 2, 4, RP, 3, true>(ctx, mode, k, t); }); break;
+    case 3: go(3, [&](int64_t t) { launch_mode<F, 32, 3, 4, RP, 2, true>(ctx, mode, k, t); }); break;
+    default: go(4, [&](int64_t t) { launch_mode<F, 32, 4, 4, RP, 2, true>(ctx, mode, k, t); }); break;
   }
 }
 
@@ -386,10 +355,21 @@ void launch_step_impl(adp_ctx* ctx, StepMode mode, const StepArgs& s);
 // neighbour needs straight into its halo over NVLink from the epilogue that computed them.
 // Other kernels (1-3 vectors, tuning variants) compute first and copy the rows out after.
 void launch_step(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
+  // operand checks for every path (the halo-push fast path below included)
+  const int epv = s.a->dtype == ADP_C128 ? 1 : 2;
+  if (s.ld % epv || s.ld_out % epv || s.ld_y % epv)
+    fail(ADP_ERR_DIMENSION, "cheb_step: leading dimension must be even for fp64");
+  auto aligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
+  if (!aligned(s.gsrc) || !aligned(s.out) || (s.vin && !aligned(s.vin)) || (s.yin && !aligned(s.yin)) ||
+      (s.wout && !aligned(s.wout)))
+    fail(ADP_ERR_DIMENSION, "cheb_step: operands must be 16-byte aligned");
+  for (int t = 0; t < s.n_push; ++t)
+    if ((reinterpret_cast<uintptr_t>(s.push[t].dst) & 15u) != 0 || s.push[t].ld_b % 16 != 0)
+      fail(ADP_ERR_DIMENSION, "cheb_step: halo push targets must be 16-byte aligned");
   if (s.n_push == 0 || s.row_end <= s.row_begin || s.q == 0) return launch_step_impl(ctx, mode, s);
   if (mode != StepMode::First && mode != StepMode::Step) fail(ADP_ERR_CONFIG, "halo push: First / Step modes only");
   if (s.n_push > kMaxPush) fail(ADP_ERR_CONFIG, "halo push: too many targets");
-  if (ctx->variant == 0 && ctx->tile_ch == 0 && launch_step_lean(ctx, mode, s)) return;
+  if (ctx->variant == 0 && launch_step_lean(ctx, mode, s)) return void(ctx->last_kernel = 2);
   StepArgs t = s;
   t.push = nullptr;
   t.n_push = 0;
@@ -403,23 +383,18 @@ void launch_step_impl(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
   const bool cplx = a->dtype == ADP_C128;
   const int epv = cplx ? 1 : 2;
-  if (s.ld % epv || s.ld_out % epv || s.ld_y % epv)
-    fail(ADP_ERR_DIMENSION, "cheb_step: leading dimension must be even for fp64");
-  auto aligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
-  if (!aligned(s.gsrc) || !aligned(s.out) || (s.vin && !aligned(s.vin)) || (s.yin && !aligned(s.yin)) ||
-      (s.wout && !aligned(s.wout)))
-    fail(ADP_ERR_DIMENSION, "cheb_step: operands must be 16-byte aligned");
   if (s.row_end <= s.row_begin || s.q == 0) return;
-  // Dispatch: the lean kernel (cheb_lean.cu) is the default for >= 4 vectors
-  // (ragged widths split into full-panel launches); the TMA tile kernel
-  // (cheb_tile.cu) when its knobs are set; the persistent pipelined row kernel
-  // (cheb_row.cu) and this file's one-row-per-group kernel as tuning variants
-  // and for 1-3 vectors.
-  if (ctx->tile_ch > 0 && launch_step_tiled(ctx, mode, s)) return;
-  if (ctx->variant >= 111 && launch_step_cube(ctx, mode, s)) return;
-  if ((ctx->variant == 0 || ctx->variant >= 81) && launch_step_line(ctx, mode, s)) return;
-  if ((ctx->variant == 0 || ctx->variant >= 21) && launch_step_lean(ctx, mode, s)) return;
-  if (ctx->variant > 10 && launch_step_row(ctx, mode, s)) return;
+  // Dispatch (variant 0 = automatic; adp_ctx_set_tuning forces one family):
+  // the plane-sweep stencil kernel (cheb_sweep.cu) for Step launches on operators that are
+  // a constant-coefficient 3-D stencil plus a diagonal; the cube / line kernels for other
+  // long-row stencils (cheb_cube.cu, cheb_line.cu); the lean kernel (cheb_lean.cu) for
+  // >= 4 vectors; this file's narrow-group row kernel for 1-3 vectors and variant 1.
+  const int v = ctx->variant;
+  if ((v == 0 || v == 5) && launch_step_sweep(ctx, mode, s)) return void(ctx->last_kernel = 5);
+  if (v == 4 && launch_step_cube(ctx, mode, s)) return void(ctx->last_kernel = 4);
+  if ((v == 0 || v == 3) && launch_step_line(ctx, mode, s)) return void(ctx->last_kernel = 3);
+  if (v != 1 && launch_step_lean(ctx, mode, s)) return void(ctx->last_kernel = 2);
+  ctx->last_kernel = 1;
   KArgs k{};
   k.row_ptr = a->row_ptr;
   k.col = a->col_idx;

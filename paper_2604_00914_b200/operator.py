@@ -61,10 +61,13 @@ class Context:
         check(lib().adp_ctx_set_panel(self.h, int(cols)))
 
     def set_tuning(self, variant: int) -> None:
+        """Kernel family: 0 automatic, 1 row, 2 lean, 3 line, 4 cube, 5 plane sweep (adp.h)."""
         check(lib().adp_ctx_set_tuning(self.h, int(variant)))
 
-    def set_tile_config(self, chunks: int = 0, stages: int = 0, stage_kib: int = 0, ctas_per_sm: int = 0) -> None:
-        check(lib().adp_ctx_set_tile_config(self.h, int(chunks), int(stages), int(stage_kib), int(ctas_per_sm)))
+    @property
+    def last_step_kernel(self) -> int:
+        """Family of the last fused-step launch (1 row, 2 lean, 3 line, 4 cube, 5 plane sweep)."""
+        return int(lib().adp_ctx_last_step_kernel(self.h))
 
 
 _default_ctx: dict[int, Context] = {}
@@ -131,6 +134,14 @@ class DeviceCsr:
     @property
     def dtype(self):
         return np.complex128 if self.is_complex else np.float64
+
+    def stencil(self) -> tuple[int, tuple[int, int, int]]:
+        """(kind, (nx, ny, nz)) if the operator is a constant-coefficient radius-1 stencil (27 box /
+        7 star; the plane-sweep kernel's precondition, verified against the CSR), else (0, (0, 0, 0))."""
+        kind = C.c_int32()
+        dims = (C.c_int64 * 3)()
+        check(lib().adp_csr_stencil(self.h, C.byref(kind), dims))
+        return int(kind.value), (int(dims[0]), int(dims[1]), int(dims[2]))
 
     def close(self):
         if getattr(self, "h", None):

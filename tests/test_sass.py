@@ -1,8 +1,8 @@
 """SASS-level checks of libadp_b200.so (CPU only: cuobjdump, no GPU).
 
 * every kernel is compiled for sm_100a;
-* the TMA tile kernel really issues bulk copies (UBLKCP), the line-ring and cube
-  kernels tensor-map tiles (UTMALDG) and the row kernels LDGSTS (cp.async);
+* the lean kernel's epilogue operands really travel by bulk copies (UBLKCP), the
+  cube and plane-sweep kernels' tiles by tensor-map copies (UTMALDG);
 * no global access uses an odd-numbered uniform descriptor register: ptxas
   12.9 produced such code for cache-hinted cp.async in one kernel shape, and
   it faults at run time (illegal instruction) -- this guards the workaround;
@@ -47,21 +47,19 @@ def test_arch_is_sm100a(sass):
 
 def test_tma_and_async_copies_present(sass):
     _, funcs = sass
-    tile = [f for f in funcs if "cheb_tile_kernel" in f]
-    assert tile and all(any("UBLKCP" in ln for ln in funcs[f]) for f in tile if "ELi1EEEv" in f)
     # cheb_lean_kernel<F, G, CH, U, MODE=1 (Step), RP, MINB>
     lean_step = [f for f in funcs if re.search(r"cheb_lean_kernelI\w+?ELi\d+ELi\d+ELi\d+ELi1E[il]Li\d+E", f)]
     assert lean_step and all(any("UBLKCP" in ln for ln in funcs[f]) for f in lean_step)
-    row_step = [f for f in funcs if "cheb_row_kernel" in f and re.search(r"ELi1E[il]Li\dELb", f)]
-    assert row_step and all(any("LDGSTS" in ln for ln in funcs[f]) for f in row_step)
-    # the pipelined line kernel moves every gathered run as a 2-D tensor-map tile (UTMALDG)
-    linep = [f for f in funcs if "cheb_linep_kernel" in f]
-    assert linep and all(any("UTMALDG" in ln for ln in funcs[f]) for f in linep)
-    pair = [f for f in funcs if "cheb_pair_kernel" in f]
-    assert pair and all(any("UBLKCP" in ln for ln in funcs[f]) for f in pair)
     # the cube kernel: gathered items (and V / Y rows) as 2-D tensor-map tiles, the block's values as a bulk copy
     cube = [f for f in funcs if "cheb_cube_kernel" in f]
     assert cube and all(any("UTMALDG" in ln for ln in funcs[f]) and any("UBLKCP" in ln for ln in funcs[f]) for f in cube)
+    # the plane sweep: W halo tiles, the diagonal and the V / Y tiles as 4-D / 3-D tensor-map tiles,
+    # consumed from shared memory (LDS), completion on mbarriers
+    sweep = [f for f in funcs if "cheb_sweep_kernel" in f]
+    assert len(sweep) == 2
+    for f in sweep:
+        assert any("UTMALDG" in ln for ln in funcs[f]) and any("LDS" in ln for ln in funcs[f])
+        assert any("SYNCS" in ln for ln in funcs[f])
 
 
 def test_no_odd_uniform_descriptors(sass):
@@ -75,9 +73,8 @@ def test_no_odd_uniform_descriptors(sass):
 def test_step_kernels_have_no_fma(sass):
     _, funcs = sass
     step = [f for f in funcs if re.search(r"cheb_\w+_kernel", f)]
-    # every fused-step design: lean, lean2, union, seg, win, pair, line, linep, row, tile, step
-    for name in ("cheb_lean_kernel", "cheb_pair_kernel", "cheb_line_kernel", "cheb_linep_kernel", "cheb_win_kernel",
-                 "cheb_cube_kernel"):
+    # every fused-step family: step (row), lean, line, cube, sweep
+    for name in ("cheb_step_kernel", "cheb_lean_kernel", "cheb_line_kernel", "cheb_cube_kernel", "cheb_sweep_kernel"):
         assert any(name in f for f in step), name
     assert step
     real = [f for f in step if "Cplx" not in f]

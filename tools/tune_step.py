@@ -22,8 +22,8 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="c2")
     p.add_argument("--degree", type=int, default=30)
-    p.add_argument("--variants", default="1", help="row-kernel variants (1-7); 0 = automatic")
-    p.add_argument("--tiles", default="", help="tile configs 'ch,stages,kib,ctas;...' (0 = default)")
+    p.add_argument("--variants", default="0,2,5", help="kernel families (adp_ctx_set_tuning): 0 automatic, 1 row, "
+                   "2 lean, 3 line, 4 cube, 5 sweep")
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--q", type=int, default=0, help="override the block width")
     p.add_argument("--panels", default="", help="lean-kernel panel caps in columns, e.g. '128,256'")
@@ -42,8 +42,6 @@ def main():
     ref = None
     b_step = bench.step_bytes(n, nnz, q, s=16 if a.is_complex else 8)
     runs = [("row", int(s), None) for s in args.variants.split(",") if s]
-    for spec in filter(None, args.tiles.split(";")):
-        runs.append(("tile", 0, [int(x) for x in spec.split(",")]))
     for spec in filter(None, args.panels.split(",")):
         runs.append(("panel", int(spec), None))
     for kind, v, tcfg in runs:
@@ -52,7 +50,6 @@ def main():
         if kind == "panel":
             v = 0
         ctx.set_tuning(v)
-        ctx.set_tile_config(*(tcfg or [0, 0, 0, 0]))
         y = torch.empty_like(x)
         adp.clenshaw_apply_device(f, da, x, args.degree, out=y)
         torch.cuda.synchronize()
@@ -68,7 +65,7 @@ def main():
             ref = y.clone()
         else:
             same = bool(torch.equal(ref, y))
-        label = {"row": f"variant {v}", "panel": f"lean panel cap {ctx_panel}"}.get(kind, f"tile ch,stages,kib,ctas={tcfg}")
+        label = {"row": f"variant {v}", "panel": f"lean panel cap {ctx_panel}"}[kind]
         print(f"{args.config} q={q} {label}: {ms:.4f} ms/launch  {b_step / ms / 1e6:.1f} GB/s  "
               f"bitwise_vs_first={same}", flush=True)
 
