@@ -2,20 +2,27 @@
 """Benchmark of the Chebyshev-filter hot path (driver contract: one JSON line on rank 0).
 
 A "step" is one ``clenshaw_apply`` call (proj/src/cheb_filter.cpp:129-179) --
-rho(l(A)) X at the configuration's initial filter degree k1 -- on config 2 of
-BASELINE.json (n = 1e6 7-point Anderson Laplacian, block q = 256, fp64), the
-largest single-GPU configuration the metric is quoted on.
+rho(l(A)) X at the configuration's initial filter degree k1 -- on config 4 of
+BASELINE.json (DFT-like 128^3 27-point stencil + Gaussian-sum potential,
+n = 2.1M, block q = 1024, fp64: 17.2 GB per block), the largest single-GPU
+HBM-bound configuration and the one north_star's scaling target names.
 
-  value  effective HBM GB/s = algorithmic bytes of the step / device time,
-         inputs resident in HBM (CUDA events on the launching stream).
+  value  effective HBM GB/s = algorithmic bytes of the call / device time,
+         inputs resident in HBM (CUDA events on the launching stream; blocks
+         far larger than the 126 MB L2, so no flush is needed).
   e2e    the same metric through the reference-facing C-ABI call
          adp_filter_apply with pinned HOST column-major X / Y (H2D + D2H and
          the layout transposes inside the timed region).
-  roofline  the fused Clenshaw-step kernel: algorithmic bytes per launch /
-         average launch duration vs the measured HBM copy bandwidth.
+  roofline  the dominant kernel (the fused Clenshaw Step launch: the
+         plane-sweep stencil kernel on configs 2 / 4): algorithmic bytes per
+         launch / its average duration measured here (a degree-2 call timed
+         and subtracted) vs the measured HBM copy bandwidth.
   cpu_baseline  the CPU oracle (faithful restatement of the reference's
          maspmm + Eigen update, OpenMP over all host threads) on a bounded
-         sample of degree steps of the same operator.
+         sample: degree steps of ONE 64-column panel, scaled by ceil(q / 64)
+         -- exact for maspmm's outer column-block loop (tiled_matrix.hpp:194).
+  solve  end-to-end solve times (the metric's second half).
+  configs  secondary lines: configs 2, 3 and 5 (device-resident filter).
 
 ``--impl reference`` times the reference's CPU path (the oracle port: the
 reference itself needs Eigen, absent here) with all host threads on the same
@@ -39,6 +46,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Chebyshev-filter SpMM effective HBM GB/s (% of peak); end-to-end solve time"  # BASELINE.json metric
+KERNELS = {1: "cheb_step_kernel (csrc/cheb_step.cu)", 2: "cheb_lean_kernel (csrc/cheb_lean.cu)",
+           3: "cheb_line_kernel (csrc/cheb_line.cu)", 4: "cheb_cube_kernel (csrc/cheb_cube.cu)",
+           5: "cheb_sweep_kernel (csrc/cheb_sweep.cu: plane-sweep stencil, 4-D TMA halo tiles)"}
 
 
 def parse_args():
@@ -47,16 +57,15 @@ def parse_args():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2")
+    p.add_argument("--config", default="c4")
     p.add_argument("--degree", type=int, default=0, help="0 = the config's initial degree k1")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU-baseline sample length")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve (second half of the metric)")
-    p.add_argument("--no-c4", action="store_true", help="skip the short config-4 (largest single-GPU stencil) measurement")
-    p.add_argument("--panel", type=int, default=0)
-    p.add_argument("--variant", type=int, default=0)
+    p.add_argument("--no-solve", action="store_true", help="skip the end-to-end solves (second half of the metric)")
+    p.add_argument("--no-secondary", action="store_true", help="skip the configs 2 / 3 / 5 lines")
+    p.add_argument("--variant", type=int, default=0, help="kernel family (adp_ctx_set_tuning); 0 = automatic")
     p.add_argument("--halo", default="p2p", choices=["p2p", "nccl"],
                    help="N > 1: halo rows stored by the step kernel into the neighbour's block over NVLink "
                         "(p2p, CUDA IPC) or exchanged with NCCL send/recv between steps")
@@ -72,6 +81,16 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def fp64_peak():
+    """Measured FP64 vector peak (profiles/fp64_peak.json, tools/fp64_peak.cu): TFLOP/s with DFMA = 2 flops."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            d = json.load(fh)
+        return float(d["dfma_tflops"]), "measured (profiles/fp64_peak.json, tools/fp64_peak.cu)"
+    except Exception:
+        return 37.0, "nominal (148 SMs x 64 FP64 lanes x 2 x 1.965 GHz)"
+
+
 def step_bytes(n, nnz, q, s=8, rp=4):
     """Algorithmic bytes of one Clenshaw degree step: A once + W, V, Y read + V write."""
     return nnz * (s + 4) + (n + 1) * rp + 4 * n * q * s
@@ -82,12 +101,24 @@ def first_bytes(n, nnz, q, s=8, rp=4):
     return nnz * (s + 4) + (n + 1) * rp + 3 * n * q * s
 
 
-def call_bytes(n, nnz, q, degree, s=8):
+def call_bytes(n, nnz, q, degree, s=8, rp=4):
     if degree >= 2:
-        return first_bytes(n, nnz, q, s) + (degree - 1) * step_bytes(n, nnz, q, s)
+        return first_bytes(n, nnz, q, s, rp) + (degree - 1) * step_bytes(n, nnz, q, s, rp)
     if degree == 1:
-        return nnz * (s + 4) + (n + 1) * 4 + 2 * n * q * s
+        return nnz * (s + 4) + (n + 1) * rp + 2 * n * q * s
     return 2 * n * q * s
+
+
+def workload(name, cfg, n, nnz, q, degree, es, world):
+    """The config dict both arms print (identical for the same --config / --degree)."""
+    return {"workload": f"{name}: {cfg.description}; clenshaw_apply degree {degree} "
+                        f"(k1 of window [{cfg.window[0]:.6g}, {cfg.window[1]:.6g}])",
+            "n": n, "nnz": nnz, "q": q, "degree": degree, "bytes_per_degree_step": step_bytes(n, nnz, q, es),
+            "bytes_per_step": call_bytes(n, nnz, q, degree, es),
+            "l2": ("inputs larger than L2 (X, W, V blocks of %.2f GB each vs 126 MB L2)" if 3 * n * q * es > 126e6
+                   else "inputs fit in L2 (X, W, V blocks of %.2f GB each; no flush: a small-config line)")
+                  % (n * q * es / 1e9),
+            "parallelism": "single GPU" if world == 1 else f"row-partition x{world}"}
 
 
 class ClockSampler:
@@ -95,7 +126,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, device: int):
         self.device = device
@@ -125,22 +156,23 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.thread.join(timeout=2)
-        sm, smax, reasons = [], [], set()
+        sm, smax, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
             try:
                 sm.append(float(parts[0]))
                 smax.append(float(parts[1]))
+                pw.append(float(parts[7]))
             except ValueError:
                 continue
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_median": statistics.median(pw) if pw else None}
 
 
 def dist_env():
@@ -150,9 +182,21 @@ def dist_env():
     return rank, world, local
 
 
+def library_mapped() -> bool:
+    """Whether this process has the product library (libadp_b200.so) mapped."""
+    try:
+        with open("/proc/self/maps") as fh:
+            return "libadp_b200.so" in fh.read()
+    except OSError:
+        return False
+
+
 # ------------------------------------------------------------- CPU legs ---
 def cpu_sample(a_csr, q: int, target_seconds: float):
-    """Time degree steps of the oracle (the reference's CPU path restated) on all host threads."""
+    """Degree steps of the oracle (the reference's CPU path restated) on all host threads, on ONE
+    column panel of min(q, 64) columns; returns (seconds per degree step at width q, steps, threads,
+    panels): the panel time x ceil(q / 64) -- maspmm's outer loop runs column blocks of T_k = 64
+    independently (tiled_matrix.hpp:194) and the array update is per element."""
     from oracle import oracle as orc
 
     orc.build()
@@ -160,119 +204,196 @@ def cpu_sample(a_csr, q: int, target_seconds: float):
     orc.set_threads(threads)
     oa = orc.Csr(a_csr.n_rows, a_csr.n_cols, a_csr.row_ptr, a_csr.col_idx, a_csr.values)
     t = orc.Tiled(oa, 256, 64)
-    sec1, _ = orc.bench_clenshaw_steps(t, q, 1)  # includes first-touch; calibrates the sample size
-    steps = max(1, min(200, int(target_seconds / max(sec1, 1e-6))))
-    sec, _ = orc.bench_clenshaw_steps(t, q, steps)
-    return sec, steps, threads
+    qs = min(q, 64)
+    panels = -(-q // 64)
+    sec1, _ = orc.bench_clenshaw_steps(t, qs, 1)  # includes first-touch; calibrates the sample size
+    steps = max(1, min(400, int(target_seconds / max(sec1, 1e-6))))
+    sec, _ = orc.bench_clenshaw_steps(t, qs, steps)
+    return sec / steps * panels, steps, threads, panels, sec
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    from oracle import oracle as orc
     from paper_2604_00914_b200 import configs
 
+    orc.build()
+    configs.set_rng(orc.uniform_range, orc.gaussian_range)  # the oracle's Philox: no product library here
     cfg = configs.CONFIGS[args.config]
+    if cfg.dtype != "f64":
+        print(json.dumps({"impl": "reference", "unavailable": f"{args.config} is complex128: the reference is "
+                          "real symmetric only (SPEC.md:15,115), there is no reference CPU path to time"}))
+        return 0
     a = cfg.operator()
     n, nnz, q = a.n_rows, a.nnz, cfg.q
     degree = args.degree or configs.filter_degree(cfg)
     b = step_bytes(n, nnz, q)
-    vals, tot_steps, threads = [], 0, 1
+    vals, secs, tot_steps, threads, panels = [], [], 0, 1, 1
     per = max(args.cpu_seconds / max(args.steps, 1), 2.0)
+    t_all = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        sec, steps, threads = cpu_sample(a, q, per if i >= args.warmup else 1.0)
+        sec_step, steps, threads, panels, sec = cpu_sample(a, q, per if i >= args.warmup else 0.5)
         if i >= args.warmup:
-            vals.append(b * steps / sec / 1e9)
+            vals.append(b / sec_step / 1e9)
+            secs.append(sec)
             tot_steps += steps
     v = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(call_bytes(n, nnz, q, degree) / (v * 1e9) * 1e3, 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {cfg.description}; clenshaw_apply degree {degree}", "n": n,
-                   "nnz": nnz, "q": q, "degree": degree, "bytes_per_degree_step": b},
+        "config": workload(args.config, cfg, n, nnz, q, degree, 8, 1),
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"{tot_steps} Clenshaw degree steps (maspmm T_i=256/T_k=64 + array update) "
-                                   f"over {args.steps} timed samples; ms_per_step projects the full degree-{degree} call"},
+                         "sample": f"each step: Clenshaw degree steps (oracle maspmm T_i=256/T_k=64 + array update, "
+                                   f"-O3 no -march, OpenMP) of ONE 64-column panel of the q={q} block, scaled by "
+                                   f"ceil(q/64) = {panels} (maspmm's column-block loop); {tot_steps} degree steps "
+                                   f"over {args.steps} timed samples; ms_per_step = one sample's wall time"},
+        "projected_ms_per_call": round(call_bytes(n, nnz, q, degree) / (v * 1e9) * 1e3, 1),
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_library_mapped": library_mapped(),
+        "wall_seconds": round(time.perf_counter() - t_all, 1),
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def end_to_end_solve(adp, configs, ctx, with_cpu: bool):
-    """End-to-end solve time (the metric's second half) on config 1 with the narrowed window (c1s).
+# ------------------------------------------------------------- solves ---
+def end_to_end_solves(adp, configs, device, with_cpu: bool):
+    """End-to-end solve time (the metric's second half).
 
-    GPU: wall time of adp.solve (setup + loop, stage split). CPU: a projection -- the oracle's
-    measured time per degree step (the reference's maspmm + update) x the GPU run's filter work
-    (sum of degree x active width, plus the k_max x 30-probe trace estimate), labelled as such.
+    c1t: a small window on a 24^3 7-point operator, solved by the GPU path AND by the CPU solver oracle
+    (oracle/solver_oracle.py: the reference's solve restated in numpy over the oracle's C++ kernels,
+    all host threads) -- both measured, same eigenvalue count, eigenvalues compared. c1s: config 1's
+    40^3 operator with a ~35-eigenvalue window on the GPU (the CPU oracle takes ~15 min there: its
+    time is projected from the measured per-step cost, labelled as such).
     """
     import torch
 
-    cfg = configs.CONFIGS["c1s"]
-    a = cfg.operator()
-    da = adp.DeviceCsr(a, ctx)
-    scfg = adp.SolverConfig(interval_a=cfg.window[0], interval_b=cfg.window[1], rng_seed=0)
-    adp.solve(da, scfg)  # warm (workspace, handles)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    res = adp.solve(da, scfg)
-    torch.cuda.synchronize()
-    gpu_s = time.perf_counter() - t0
-    out = {"config": "c1s: " + cfg.description, "n": a.n_rows, "window": list(cfg.window),
-           "gpu_seconds": round(gpu_s, 4), "converged": res.converged, "n_eigs": int(len(res.eigenvalues)),
-           "iterations": res.iterations, "spmv_total": res.spmv_total, "avg_degree": round(res.avg_degree, 1),
-           "max_residual": res.max_residual, "subspace_dim": res.subspace_dim,
-           "stage_seconds": {k: round(v, 4) for k, v in vars(res.timings).items()}}
-    if with_cpu:
-        # columns x degree-steps of filter work in the GPU run, including the setup trace estimate
-        k1 = configs.filter_degree(configs.Config("tmp", "", 0, cfg.window,
-                                                  (res.bounds.lambda_min, res.bounds.lambda_max), "f64", None))
-        k_max = max(k1, int(math.ceil(2.5 * k1)))
-        col_steps = k_max * 30 + sum(r.degree * r.active_width for r in res.history)
-        sec, steps, threads = cpu_sample(a, 64, 4.0)
-        per_col_step = sec / steps / 64
-        out["cpu_projected_seconds"] = round(col_steps * per_col_step, 2)
-        out["cpu_projection"] = (f"oracle degree-step time ({steps} steps at q=64, {threads} threads: "
-                                 f"{1e3 * sec / steps:.2f} ms) x {col_steps} column-steps of the GPU run's filter work")
+    out = {}
+    ctx = adp.Context(device)
+    for name in ("c1t", "c1s"):
+        cfg = configs.CONFIGS[name]
+        a = cfg.operator()
+        da = adp.DeviceCsr(a, ctx)
+        scfg = adp.SolverConfig(interval_a=cfg.window[0], interval_b=cfg.window[1], rng_seed=0)
+        adp.solve(da, scfg)  # warm (workspace, handles)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = adp.solve(da, scfg)
+        torch.cuda.synchronize()
+        gpu_s = time.perf_counter() - t0
+        d = {"config": f"{name}: " + cfg.description, "n": a.n_rows, "window": list(cfg.window),
+             "gpu_seconds": round(gpu_s, 4), "converged": res.converged, "n_eigs": int(len(res.eigenvalues)),
+             "iterations": res.iterations, "spmv_total": res.spmv_total, "avg_degree": round(res.avg_degree, 1),
+             "max_residual": res.max_residual, "subspace_dim": res.subspace_dim,
+             "stage_seconds": {k: round(v, 4) for k, v in vars(res.timings).items()}}
+        if with_cpu and name == "c1t":
+            from oracle import oracle as orc
+            from oracle import solver_oracle
+
+            orc.build()
+            orc.set_threads(orc.max_threads())
+            oa = orc.Csr(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)
+            t0 = time.perf_counter()
+            cres = solver_oracle.solve(oa, cfg.window[0], cfg.window[1], rng_seed=0)
+            cpu_s = time.perf_counter() - t0
+            ge, ce = np.sort(res.eigenvalues), np.sort(cres.eigenvalues)
+            d["cpu_seconds"] = round(cpu_s, 3)
+            d["cpu_threads"] = orc.max_threads()
+            d["cpu_n_eigs"] = int(len(ce))
+            d["eigenvalues_max_rel_diff_vs_cpu"] = (float(np.max(np.abs(ge - ce) / np.maximum(np.abs(ce), 1e-300)))
+                                                    if len(ge) == len(ce) and len(ce) else None)
+            d["cpu_solver"] = "oracle/solver_oracle.py (the reference's solve restated; measured, not projected)"
+        if with_cpu and name == "c1s":
+            k1 = configs.filter_degree(configs.Config("tmp", "", 0, cfg.window,
+                                                      (res.bounds.lambda_min, res.bounds.lambda_max), "f64", None))
+            k_max = max(k1, int(math.ceil(2.5 * k1)))
+            col_steps = k_max * 30 + sum(r.degree * r.active_width for r in res.history)
+            sec_step, steps, threads, _, _ = cpu_sample(a, 64, 4.0)
+            d["cpu_projected_seconds"] = round(col_steps * sec_step / 64, 2)
+            d["cpu_projection"] = (f"PROJECTION: oracle degree-step time (q=64, {threads} threads: "
+                                   f"{1e3 * sec_step:.2f} ms) x {col_steps} column-steps of the GPU run's filter work")
+        out[name] = d
+        da.close()
+    ctx.close()
     return out
 
 
 # ------------------------------------------------------------- GPU arm ---
-def largest_config(adp, configs, ctx, peak):
-    """Config 4 (128^3 27-point stencil, q = 1024 fp64: 17.2 GB per block), a short device-resident
-    clenshaw_apply after the main measurement: the cube kernel (csrc/cheb_cube.cu) on its full panels.
-    Reported beside the headline, not part of it (its own operator, degree and timing)."""
+def time_filter(adp, da, f, x, y, degree, reps, stream):
     import torch
 
-    cfg = configs.CONFIGS["c4"]
-    a = cfg.operator()
-    n, nnz, q = a.n_rows, a.nnz, cfg.q
-    k1 = configs.filter_degree(cfg)
-    f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, int(math.ceil(2.5 * k1)), 0.5)
-    da = adp.DeviceCsr(a, ctx)
-    x = torch.randn(n, q, dtype=torch.float64, device="cuda", generator=torch.Generator(device="cuda").manual_seed(0))
-    y = torch.empty_like(x)
-    deg = 24
-    adp.clenshaw_apply_device(f, da, x, 4, out=y)  # operator plans + workspace
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(2):
-        adp.clenshaw_apply_device(f, da, x, deg, out=y)
+    for _ in range(reps):
+        adp.clenshaw_apply_device(f, da, x, degree, out=y)
     ev1.record(stream)
     torch.cuda.synchronize()
-    ms_launch = ev0.elapsed_time(ev1) / (2 * deg)
-    b_step = step_bytes(n, nnz, q)
-    gbs = b_step / (ms_launch * 1e-3) / 1e9
-    da.close()
-    del x, y
-    torch.cuda.empty_cache()
-    return {"workload": f"c4: {cfg.description}; 2 x clenshaw_apply degree {deg}, inputs resident",
-            "n": n, "nnz": nnz, "q": q, "bytes_per_degree_step": b_step, "ms_per_degree_step": round(ms_launch, 4),
-            "value": round(gbs, 3), "unit": "GB/s", "frac_of_hbm_peak": round(gbs / peak, 4),
-            "kernel": "cheb_cube_kernel (csrc/cheb_cube.cu) on the full 64-vector panels"}
+    return ev0.elapsed_time(ev1) / reps
+
+
+def secondary(adp, configs, device, peak, fpk):
+    """Configs 2, 3 and 5: device-resident clenshaw_apply lines beside the headline (each on a fresh
+    context; its own operator, degree and timing)."""
+    import torch
+
+    from paper_2604_00914_b200 import _native
+    import ctypes as C
+
+    out = {}
+    plans = [("c2", None, "the configuration's k1, one call"), ("c3", 400, "400 degree steps of its k1 = 6999"),
+             ("c5", 8, "8 degree steps (k1 = 17948 would take ~3 h); operator generated on the GPU")]
+    for name, deg_override, note in plans:
+        cfg = configs.CONFIGS[name]
+        ctx = adp.Context(device)
+        stream = torch.cuda.current_stream()
+        ctx.set_stream(stream)
+        t0 = time.perf_counter()
+        da = cfg.device_operator(ctx)
+        build_s = time.perf_counter() - t0
+        n, nnz, q = da.n_rows, da.nnz, cfg.q
+        cplx = cfg.dtype == "c128"
+        es = 16 if cplx else 8
+        rp = 8 if nnz >= 2 ** 31 else 4
+        k1 = configs.filter_degree(cfg)
+        degree = deg_override or k1
+        f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, max(degree, int(math.ceil(2.5 * k1))), 0.5)
+        x = torch.empty(n, q, dtype=torch.complex128 if cplx else torch.float64, device="cuda")
+        qr = 2 * q if cplx else q
+        _native.check(_native.lib().adp_fill_gaussian_device(ctx.h, C.c_void_p(x.data_ptr()), n, qr, qr, 0, 0))
+        y = torch.empty_like(x)
+        adp.clenshaw_apply_device(f, da, x, 3, out=y)  # plans + workspace
+        torch.cuda.synchronize()
+        clocks = ClockSampler(device)
+        clocks.start()
+        ms_call = time_filter(adp, da, f, x, y, degree, 1, stream)
+        t2 = time_filter(adp, da, f, x, y, 2, 2, stream)
+        clk = clocks.stop()
+        kern = ctx.last_step_kernel
+        launch_ms = (ms_call - t2) / (degree - 2)
+        b_step = step_bytes(n, nnz, q, es, rp)
+        gbs = call_bytes(n, nnz, q, degree, es, rp) / (ms_call * 1e-3) / 1e9
+        d = {"workload": f"{name}: {cfg.description}; clenshaw_apply degree {degree} ({note})",
+             "n": n, "nnz": nnz, "q": q, "dtype": cfg.dtype, "degree": degree, "ms_per_call": round(ms_call, 3),
+             "value": round(gbs, 2), "unit": "GB/s", "frac_of_hbm_peak": round(gbs / peak, 4),
+             "step_kernel": KERNELS.get(kern), "step_launch_ms": round(launch_ms, 4),
+             "step_kernel_gbs": round(b_step / (launch_ms * 1e-3) / 1e9, 2), "operator_seconds": round(build_s, 1),
+             "clocks": clk}
+        if name == "c5":  # FP64- and gather-bound (SURVEY.md 8d): the FP64 roofline against the measured peak
+            flops = 8 * nnz * q + 12 * n * q
+            d["fp64_tflops"] = round(flops / (launch_ms * 1e-3) / 1e12, 2)
+            d["fp64_peak_tflops"], d["fp64_peak_source"] = fpk
+            d["frac_of_fp64_peak"] = round(d["fp64_tflops"] / fpk[0], 4)
+            d["note"] = ("complex MAC = 4 DFMA (8 flops); bound = max(FP64, gather-inflated HBM): ~40 random off-band "
+                         "W rows per output row miss L2 (DESIGN.md 3.1)")
+        out[name] = d
+        del x, y
+        da.close()
+        ctx.close()
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(args):
@@ -291,29 +412,26 @@ def run_ours(args):
     from paper_2604_00914_b200 import configs
 
     cfg = configs.CONFIGS[args.config]
-    a = cfg.operator()
-    n, nnz, q = a.n_rows, a.nnz, cfg.q
+    a = cfg.operator() if cfg.dtype == "f64" or world > 1 else None
     k1 = configs.filter_degree(cfg)
     degree = args.degree or k1
     k_max = max(degree, int(math.ceil(2.5 * k1)))
     f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, k_max, 0.5)
     if world > 1 or os.environ.get("ADP_BENCH_FORCE_DIST") == "1":
-        return run_distributed(args, adp, cfg, a, f, degree, rank, world, device)
+        return run_distributed(args, adp, configs, cfg, a, f, degree, rank, world, device)
 
-    # complex128 configurations (3, 5s): 16-byte values and block elements; the e2e, CPU-baseline and
-    # solve legs are real-only, so a complex line carries the device-resident measurement alone
     cplx = cfg.dtype == "c128"
     es = 16 if cplx else 8
     if cplx:
-        args.no_e2e = args.no_cpu_baseline = args.no_solve = args.no_c4 = True
+        args.no_e2e = args.no_cpu_baseline = True
     ctx = adp.Context(device)
-    if args.panel:
-        ctx.set_panel(args.panel)
     if args.variant:
         ctx.set_tuning(args.variant)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream)
-    da = adp.DeviceCsr(a, ctx)
+    da = adp.DeviceCsr(a, ctx) if a is not None else cfg.device_operator(ctx)
+    n, nnz, q = da.n_rows, da.nnz, cfg.q
+    rp = 8 if nnz >= 2 ** 31 else 4
     x = torch.empty(n, q, dtype=torch.complex128 if cplx else torch.float64, device="cuda")
     from paper_2604_00914_b200 import _native
     import ctypes as C
@@ -322,44 +440,39 @@ def run_ours(args):
     _native.check(_native.lib().adp_fill_gaussian_device(ctx.h, C.c_void_p(x.data_ptr()), n, qr, qr, 0, 0))
     y = torch.empty_like(x)
 
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-
     for _ in range(args.warmup):
         adp.clenshaw_apply_device(f, da, x, degree, out=y)
-    barrier()
+    torch.cuda.synchronize()
     clocks = ClockSampler(device)
     clocks.start()
     launches0 = ctx.launch_count
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    barrier()
+    torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(args.steps):
         adp.clenshaw_apply_device(f, da, x, degree, out=y)
     ev1.record(stream)
-    barrier()
+    torch.cuda.synchronize()
     clk = clocks.stop()
     ms_total = ev0.elapsed_time(ev1)
     launches = ctx.launch_count - launches0
-    if world > 1:
-        t = torch.tensor([ms_total], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_total = float(t.item())
+    kern = ctx.last_step_kernel
     ms_step = ms_total / args.steps
-    bytes_call = call_bytes(n, nnz, q, degree, es)
-    value = world * bytes_call / (ms_step * 1e-3) / 1e9
-    b_step = step_bytes(n, nnz, q, es)
-    launch_ms = ms_step / max(degree, 1)  # every launch of the call is one fused step kernel
+    bytes_call = call_bytes(n, nnz, q, degree, es, rp)
+    value = bytes_call / (ms_step * 1e-3) / 1e9
+    b_step = step_bytes(n, nnz, q, es, rp)
+    # the dominant kernel's average launch: the call's Step launches (degree - 1 of them: First + Steps),
+    # isolated by timing degree-2 calls (First + one Step) on the same stream and subtracting
+    t2 = time_filter(adp, da, f, x, y, 2, 3, stream) if degree > 2 else None
+    launch_ms = (ms_step - t2) / (degree - 2) if t2 is not None else ms_step / max(degree, 1)
     achieved = b_step / (launch_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{args.config}/q{q}")
+            traffic = json.load(open(tpath)).get(f"{args.config}/q{q}/{kern}")
         except Exception:
             traffic = None
 
@@ -367,10 +480,8 @@ def run_ours(args):
     if not args.no_e2e:
         # Reference-facing call: host column-major X (Eigen layout) in pinned memory -> adp_filter_apply.
         xh = torch.empty((q, n), dtype=torch.float64).pin_memory()  # (q, n) C-order == (n, q) column-major
-        xh.copy_(x.t().cpu())
+        xh.copy_(x.t())
         yh = torch.empty((q, n), dtype=torch.float64).pin_memory()
-        import ctypes as C
-
         lib = _native.lib()
         coeffs = f.coeff_array()
         cnt = C.c_int64(0)
@@ -381,78 +492,74 @@ def run_ours(args):
                                                C.c_void_p(yh.data_ptr()), n, C.byref(cnt)))
 
         e2e_call()  # warm (workspace allocation)
-        barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_call()
-        barrier()
+        torch.cuda.synchronize()
         t_e2e = (time.perf_counter() - t0) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([t_e2e], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            t_e2e = float(t.item())
-        # sanity: the host result equals the device result of the same call
-        same = bool(torch.equal(yh.t().to("cuda"), y))
-        e2e = {"value": round(world * bytes_call / t_e2e / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n * q * 8,
+        same = bool(torch.equal(yh.t().to("cuda"), y))  # the host result equals the device result of the same call
+        e2e = {"value": round(bytes_call / t_e2e / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n * q * 8,
                "d2h_bytes_per_step": n * q * 8, "ms_per_step": round(t_e2e * 1e3, 3), "matches_device_result": same,
                "api": "adp_filter_apply (C-ABI, host column-major, pinned)"}
-
-    solve_info = None
-    if rank == 0 and not args.no_solve:
-        solve_info = end_to_end_solve(adp, configs, ctx, with_cpu=(world == 1 and not args.no_cpu_baseline))
-
-    c4 = None
-    if rank == 0 and world == 1 and not args.no_c4 and args.config == "c2":
-        del x, y
-        torch.cuda.empty_cache()
-        c4 = largest_config(adp, configs, ctx, peaks()[0])
+        del xh, yh
+    del x, y
+    da.close()
+    ctx.close()
+    torch.cuda.empty_cache()
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sec, steps, threads = cpu_sample(a, q, args.cpu_seconds)
-        cpu = {"value": round(b_step * steps / sec / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{steps} Clenshaw degree steps of the same operator (oracle maspmm T_i=256/T_k=64 + "
-                         f"array update, OpenMP, -O3 no -march), {sec:.1f} s"}
+    if not args.no_cpu_baseline:
+        sec_step, steps, threads, panels, sec = cpu_sample(a, q, args.cpu_seconds)
+        cpu = {"value": round(b_step / sec_step / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": f"{steps} Clenshaw degree steps of one 64-column panel of the same operator (oracle maspmm "
+                         f"T_i=256/T_k=64 + array update, OpenMP, -O3 no -march), {sec:.1f} s, scaled by "
+                         f"ceil(q/64) = {panels}"}
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128" if cplx else "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfg.description}; clenshaw_apply degree {degree} "
-                                   f"(k1 of window [{cfg.window[0]:.6g}, {cfg.window[1]:.6g}])",
-                       "n": n, "nnz": nnz, "q": q, "degree": degree, "bytes_per_degree_step": b_step,
-                       "bytes_per_step": bytes_call,
-                       "l2": ("inputs larger than L2 (X, W, V blocks of %.2f GB each vs 126 MB L2)" if 3 * n * q * es > 126e6
-                              else "inputs fit in L2 (X, W, V blocks of %.2f GB each; no flush: a small-config line)")
-                             % (n * q * es / 1e9),
-                       "parallelism": "single GPU" if world == 1 else f"replicas x{world}"},
-            "pct_of_hbm_peak": round(100.0 * value / world / peak, 2),
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "cheb_lean_kernel (fused Clenshaw step, csrc/cheb_lean.cu)",
-                         "peak_source": peak_src,
-                         "launch_ms": round(launch_ms, 5)},
-            "gpu_launches": launches,
-            "clocks": clk,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "solve": solve_info,
-            "largest_config": c4,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    solve_info = None
+    if not args.no_solve:
+        solve_info = end_to_end_solves(adp, configs, device, with_cpu=not args.no_cpu_baseline)
+
+    extra = None
+    if not args.no_secondary:
+        extra = secondary(adp, configs, device, peak, fp64_peak())
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128" if cplx else "f64", "data": "synthetic",
+        "config": workload(args.config, cfg, n, nnz, q, degree, es, world),
+        "pct_of_hbm_peak": round(100.0 * value / peak, 2),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": KERNELS.get(kern), "peak_source": peak_src, "launch_ms": round(launch_ms, 5),
+                     "launch_timing": "average Step launch: (degree-d call - degree-2 call) / (d - 2), CUDA events "
+                                      "on the launching stream"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "solve": solve_info,
+        "configs": extra,
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 
-def run_distributed(args, adp, cfg, a, f, degree, rank, world, device):
-    """N > 1: the filter row-partitioned over the ranks (strong scaling: the operator is fixed).
-    Default (--halo p2p): the step kernel stores the rows each neighbour needs straight into the
-    neighbour's block over NVLink (CUDA IPC mappings) and publishes a counter; the neighbour's next
-    step waits on it (PeerHaloFilter). --halo nccl: NCCL send/recv of the halo rows between steps
-    while interior rows compute (DistributedFilter). If the peer-memory setup fails on a box, the
-    NCCL exchange is used and the JSON line says so (paper_2604_00914_b200/distributed.py)."""
+def plane_ranges(n_rows: int, plane: int, world: int):
+    """Contiguous row ranges on grid-plane boundaries (the sweep kernel's interior slabs)."""
+    planes = n_rows // plane
+    cuts = [round(k * planes / world) * plane for k in range(world + 1)]
+    return [(cuts[k], cuts[k + 1]) for k in range(world)]
+
+
+def run_distributed(args, adp, configs, cfg, a, f, degree, rank, world, device):
+    """N > 1: the filter row-partitioned over the ranks (strong scaling: the operator is fixed), in
+    slabs of whole grid planes for stencil operators. Default (--halo p2p): the step kernel stores the
+    rows each neighbour needs straight into the neighbour's block over NVLink (CUDA IPC mappings) and
+    publishes a counter; the neighbour's next step waits on it (PeerHaloFilter). --halo nccl: NCCL
+    send/recv of the halo rows between steps while interior rows compute (DistributedFilter). If the
+    peer-memory setup fails on a box, the NCCL exchange is used and the JSON line says so."""
     import torch
     import torch.distributed as dist
 
@@ -461,7 +568,10 @@ def run_distributed(args, adp, cfg, a, f, degree, rank, world, device):
     n, nnz, q = a.n_rows, a.nnz, cfg.q
     ctx = adp.Context(device)
     be = CudaStepBackend(ctx)
-    ranges = None
+    da0 = adp.DeviceCsr(a, ctx)
+    kind, dims = da0.stencil()
+    da0.close()
+    ranges = plane_ranges(n, dims[0] * dims[1], world) if kind else None
     g = torch.Generator(device="cuda").manual_seed(rank)
 
     def barrier():
@@ -473,7 +583,7 @@ def run_distributed(args, adp, cfg, a, f, degree, rank, world, device):
     df = None
     if halo == "p2p":
         try:
-            df = PeerHaloFilter(a, be, rank, world, IpcPeerDirectory(), timeout_ms=30000)
+            df = PeerHaloFilter(a, be, rank, world, IpcPeerDirectory(), ranges=ranges, timeout_ms=30000)
             r0, r1 = df.ranges[rank]
             x = torch.randn(r1 - r0, q, dtype=torch.float64, device="cuda", generator=g)
             df.apply(f.coeffs, f.l1, f.l2, x, min(degree, 3))
@@ -501,7 +611,7 @@ def run_distributed(args, adp, cfg, a, f, degree, rank, world, device):
     barrier()
     ev0.record()
     for _ in range(args.steps):
-        y = df.apply(f.coeffs, f.l1, f.l2, x, degree)
+        df.apply(f.coeffs, f.l1, f.l2, x, degree)
     ev1.record()
     barrier()
     clk = clocks.stop()
@@ -516,35 +626,35 @@ def run_distributed(args, adp, cfg, a, f, degree, rank, world, device):
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            yh = df.apply(f.coeffs, f.l1, f.l2, xh.to("cuda", non_blocking=True), degree).to("cpu")
+            df.apply(f.coeffs, f.l1, f.l2, xh.to("cuda", non_blocking=True), degree).to("cpu")
         barrier()
         te = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], device="cuda")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(bytes_call / float(te.item()) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": n * q * 8, "d2h_bytes_per_step": n * q * 8,
-               "api": "DistributedFilter.apply (host tensors in/out)"}
+               "api": "PeerHaloFilter / DistributedFilter.apply (host tensors in/out)"}
     peak, peak_src = peaks()
-    # per-GPU roofline of the step kernel: this rank's share of the algorithmic bytes per degree
-    # step over the time of one degree step (interior + boundary launches)
+    # per-GPU roofline of the step: this rank's share of the algorithmic bytes per degree step over the
+    # time of one degree step (interior + boundary launches)
     step_ms = ms_step / max(degree, 1)
     achieved = step_bytes(n, nnz, q) / world / (step_ms * 1e-3) / 1e9
     if rank == 0:
+        conf = workload(args.config, cfg, n, nnz, q, degree, 8, world)
+        conf["parallelism"] = (f"row-partition x{world} ("
+                               + ("halo stored by the step kernel into peer memory over NVLink" if halo == "p2p"
+                                  else "NCCL halo send/recv") + ")")
+        conf["halo"] = halo
+        conf["slabs"] = "whole grid planes" if ranges else "balanced rows"
+        if note:
+            conf["halo_note"] = note
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": "cheb_lean_kernel (per-GPU share, interior + boundary launches)",
+                         "kernel": "per-GPU share: interior slab (sweep kernel) + boundary planes (halo push)",
                          "peak_source": peak_src, "degree_step_ms": round(step_ms, 5)},
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfg.description}; clenshaw_apply degree {degree}, "
-                                   f"rows partitioned over {world} GPUs, halo exchange per degree step",
-                       "n": n, "nnz": nnz, "q": q, "degree": degree, "bytes_per_step": bytes_call,
-                       "l2": "inputs larger than L2",
-                       "parallelism": f"row-partition x{world} ("
-                                      + ("halo stored by the step kernel into peer memory over NVLink" if halo == "p2p"
-                                         else "NCCL halo send/recv") + ")",
-                       "halo": halo, **({"halo_note": note} if note else {})},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": conf,
             "pct_of_hbm_peak_per_gpu": round(100.0 * value / world / peak, 2),
             "gpu_launches": ctx.launch_count - launches0, "clocks": clk, "e2e": e2e, "cpu_baseline": None,
         }

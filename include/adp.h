@@ -233,6 +233,9 @@ adp_status adp_fill_rademacher_device(adp_ctx* ctx, double* d_out, int64_t n, in
                                       uint64_t seed, uint64_t stream);
 
 /* ------------------------------------------------- device solver subsystems -- */
+/* csr_spmv (include/adapoly/csr_matrix.hpp:122-134): y = A x for real A, one row per thread,
+ * products accumulated sequentially in CSR order (the Lanczos SpMV); device x, y. */
+adp_status adp_spmv_device(adp_ctx* ctx, const adp_csr* a, const double* d_x, double* d_y);
 /* estimate_spectrum_bounds (include/adapoly/lanczos.hpp:24-26, src/lanczos.cpp:81-111):
  * 40-step Lanczos with full reorthogonalisation on the device. */
 adp_status adp_lanczos_bounds(adp_ctx* ctx, const adp_csr* a, int32_t steps, uint64_t seed, double* lambda_min,

@@ -10,8 +10,8 @@ from .bounds import (c_m_constant, damped_bound, inspect_filter, inspect_filter_
                      undamped_bound)
 from .filter import (ChebFilter, SpectrumBounds, adaptive_degree, build_filter, chebyshev_step_coeffs,
                      eval_filter_scalar, initial_degree, jackson_damping, lanczos_damping)
-from .operator import (Context, DeviceCsr, clenshaw_apply, clenshaw_apply_device, default_context, maspmm,
-                       maspmm_device)
+from .operator import (Context, DeviceCsr, clenshaw_apply, clenshaw_apply_device, csr_spmv_device, default_context,
+                       maspmm, maspmm_device)
 from .hermitian import hermitian_embedding, solve_hermitian
 from .report import RunReport, dump_report, run_report_from_json, run_solve, to_json
 from .slicing import SlicedResult, balanced_slices, slice_interval, solve_sliced
@@ -29,7 +29,7 @@ __all__ = [
     "AdpError", "CollectiveError", "ConfigError", "CudaError", "DimensionError", "NotPositiveDefinite",
     "OutOfMemory", "ParseError", "lib", "ChebFilter", "SpectrumBounds", "adaptive_degree", "build_filter",
     "chebyshev_step_coeffs", "eval_filter_scalar", "initial_degree", "jackson_damping", "lanczos_damping",
-    "Context", "DeviceCsr", "clenshaw_apply", "clenshaw_apply_device", "default_context", "maspmm",
+    "Context", "DeviceCsr", "clenshaw_apply", "clenshaw_apply_device", "csr_spmv_device", "default_context", "maspmm",
     "maspmm_device", "CsrMatrix", "fill_gaussian", "fill_rademacher", "parse_matrix_market", "philox_block",
     "philox_gaussian", "philox_uniform", "read_matrix_market", "IterationRecord", "SolveResult", "SolverConfig",
     "StageTimings", "cholesky_qr_device", "compute_residuals_device", "estimate_eigcount",

@@ -88,6 +88,7 @@ SIGNATURES = {
     "adp_ctx_launch_count": (I64, [P]),
     "adp_ctx_last_step_kernel": (I32, [P]),
     "adp_csr_stencil": (I32, [P, P, P]),
+    "adp_spmv_device": (I32, [P, P, P, P]),
     "adp_ctx_set_panel": (I32, [P, I32]),
     "adp_ctx_set_tuning": (I32, [P, I32]),
     "adp_csr_create": (I32, [P, I64, I64, P, P, P, I32, P]),

@@ -22,6 +22,25 @@ STREAM_POTENTIAL = 16
 STREAM_CENTRES = 17
 STREAM_OFFBAND = 18
 
+# The Philox4x32-10 draws behind the generators (sparse.philox_uniform / philox_gaussian, the
+# library's restatement of philox.hpp). set_rng swaps in another implementation of the same
+# streams -- bench.py's reference arm builds its operator with the CPU oracle's Philox so that
+# arm never maps the product library; tests pin the two bitwise.
+_RNG = {"uniform": None, "gaussian": None}
+
+
+def set_rng(uniform=None, gaussian=None) -> None:
+    """Use uniform(seed, stream, first, count) / gaussian(...) for matrix randomness (None: the library's)."""
+    _RNG["uniform"], _RNG["gaussian"] = uniform, gaussian
+
+
+def _uniform(seed, stream, first, count):
+    return (_RNG["uniform"] or philox_uniform)(seed, stream, first, count)
+
+
+def _gaussian(seed, stream, first, count):
+    return (_RNG["gaussian"] or philox_gaussian)(seed, stream, first, count)
+
 
 def _assemble(n: int, cols: np.ndarray, vals: np.ndarray, valid: np.ndarray) -> CsrMatrix:
     """Rows given as fixed-width candidate lists (already ascending per row) + validity mask."""
@@ -74,7 +93,7 @@ def _twenty_seven_point():
 def laplacian7_potential(nx: int, lo: float, hi: float, seed: int = 0) -> CsrMatrix:
     """7-point -Laplacian (diag 6, off -1) + diagonal potential uniform [lo, hi) (configs 1, 2)."""
     n = nx ** 3
-    u = philox_uniform(seed, STREAM_POTENTIAL, 0, n)
+    u = _uniform(seed, STREAM_POTENTIAL, 0, n)
     offs, ws = _seven_point()
     return stencil_3d(nx, offs, ws, 6.0 + (lo + (hi - lo) * u))
 
@@ -82,7 +101,7 @@ def laplacian7_potential(nx: int, lo: float, hi: float, seed: int = 0) -> CsrMat
 def dft_like_27pt(nx: int = 128, n_centres: int = 64, seed: int = 0) -> CsrMatrix:
     """27-point compact stencil + smooth Gaussian-sum local potential (config 4)."""
     n = nx ** 3
-    cen = philox_uniform(seed, STREAM_CENTRES, 0, 3 * n_centres).reshape(n_centres, 3) * nx
+    cen = _uniform(seed, STREAM_CENTRES, 0, 3 * n_centres).reshape(n_centres, 3) * nx
     idx = np.arange(n, dtype=np.int64)
     pts = np.stack([idx % nx, (idx // nx) % nx, idx // (nx * nx)], axis=1).astype(np.float64)
     pot = np.zeros(n)
@@ -102,7 +121,7 @@ def peierls_lattice(L: int = 1000, phi: float = 1.0 / 64.0, seed: int = 0) -> Cs
     n = L * L
     idx = np.arange(n, dtype=np.int64)
     x, y = idx % L, idx // L
-    onsite = -1.0 + 2.0 * philox_uniform(seed, STREAM_POTENTIAL, 0, n)
+    onsite = -1.0 + 2.0 * _uniform(seed, STREAM_POTENTIAL, 0, n)
     ph = np.exp(2j * math.pi * phi * x)
     cols = np.stack([idx - L, idx - 1, idx, idx + 1, idx + L], axis=1)
     vals = np.stack([-np.conj(ph), -np.ones(n), onsite.astype(np.complex128), -np.ones(n), -ph], axis=1)
@@ -120,7 +139,7 @@ def random_banded_hermitian(n: int, half_band: int, offband: int, seed: int = 0)
         i = np.arange(0, n - d, dtype=np.int64)
         rows.append(i)
         cols.append(i + d)
-    u = philox_uniform(seed, STREAM_OFFBAND, 0, n * offband)
+    u = _uniform(seed, STREAM_OFFBAND, 0, n * offband)
     r_off = np.repeat(np.arange(n, dtype=np.int64), offband)
     c_off = np.minimum((u * n).astype(np.int64), n - 1)
     keep = np.abs(c_off - r_off) > half_band
@@ -129,7 +148,7 @@ def random_banded_hermitian(n: int, half_band: int, offband: int, seed: int = 0)
     cols.append(hi)
     key = np.unique(np.concatenate(rows) * n + np.concatenate(cols))
     r, c = key // n, key % n
-    g = philox_gaussian(seed, STREAM_OFFBAND + 1, 0, 2 * len(r)) * np.sqrt(0.5)
+    g = _gaussian(seed, STREAM_OFFBAND + 1, 0, 2 * len(r)) * np.sqrt(0.5)
     v = g[0::2] + 1j * g[1::2]
     v[r == c] = v[r == c].real
     off = r != c
@@ -269,6 +288,12 @@ CONFIGS = {
     "c1s": Config("c1s", "3D 7-pt Laplacian 40^3 + U[0,1) potential, solve window ~35 eigenvalues", 64,
                   (0.425 * 13.0 - 0.002, 0.425 * 13.0 + 0.002), (0.0, 13.0), "f64",
                   lambda: laplacian7_potential(40, 0.0, 1.0)),
+    # A SMALL replica of config 1 for the bench's measured CPU-vs-GPU solve: 16^3 grid, same potential
+    # distribution, window of ~24 eigenvalues at 0.425 of the range (the CPU solver oracle takes ~10 s on
+    # 8 host threads; c1s takes ~15 min there).
+    "c1t": Config("c1t", "3D 7-pt Laplacian 16^3 + U[0,1) potential, solve window ~24 eigenvalues", 64,
+                  (0.425 * 13.0 - 0.02, 0.425 * 13.0 + 0.02), (0.0, 13.0), "f64",
+                  lambda: laplacian7_potential(16, 0.0, 1.0)),
     # bounds: the Gershgorin enclosure [-5.885, 8.533] (the 64 wells of depth 2 overlap down to -5.9;
     # Lanczos: [-5.47, 6.16]). An earlier (-2.0, 8.6) missed the wells' bottom: the filter diverged at
     # high degree (the trace estimate at k_max = 765 returned NaN); low-degree timings were unaffected.

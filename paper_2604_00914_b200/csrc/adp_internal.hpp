@@ -122,7 +122,9 @@ namespace adp {
 struct StencilPlan {
   bool valid = false;
   int kind = 0;               // 27 (box) or 7 (star)
-  int64_t nx = 0, ny = 0, nz = 0;
+  int64_t nx = 0, ny = 0, nz = 0;  // nz: planes of the operator's rows
+  int64_t nzw = 0;            // planes of the grid its columns index (> nz for a rank's halo-extended rows)
+  int64_t goff = 0;           // row r is point r + goff of that grid
   int64_t nxp = 0;            // x pitch of the diagonal array (even: 16-byte rows for TMA)
   double w[27] = {};          // value at offset (dx, dy, dz): index (dz+1)*9 + (dy+1)*3 + (dx+1); centre unused
   double* d_diag = nullptr;   // [nz][ny][nxp] centre values
@@ -236,7 +238,7 @@ const CubePlan* get_cube_plan(adp_csr* a, int rows_per_line, int ly, int lz, int
 // The plane-sweep stencil kernel (cheb_sweep.cu): Step launches on constant-coefficient 3-D stencil
 // operators (StencilPlan). Returns false if not applicable.
 bool launch_step_sweep(adp_ctx* ctx, StepMode mode, const StepArgs& args);
-const StencilPlan* get_stencil_plan(adp_csr* a);
+const StencilPlan* get_stencil_plan(adp_csr* a, int64_t goff = 0);
 // Host copies of a device-created operator's arrays, downloaded on first use by the
 // host-side preprocessing (line plans, tilings, segments, the dense fallback).
 void ensure_host_copy(adp_csr* a);

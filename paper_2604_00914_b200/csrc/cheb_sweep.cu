@@ -62,10 +62,13 @@ struct Off {
   int dx, dy, dz;
 };
 
-void build_stencil_plan(adp_csr* a, StencilPlan& p) {
-  const int64_t n = a->n_rows;
+// Row r of the operator is grid point g = r + goff of an extended grid whose points are the operator's
+// columns (goff != 0: a rank's rows of the row partition, columns in its halo-extended local layout).
+void build_stencil_plan(adp_csr* a, int64_t goff, StencilPlan& p) {
+  const int64_t n = a->n_rows, nc = a->n_cols;
+  p.goff = goff;
   if (a->dtype != ADP_F64) return void(p.why = "not real fp64");
-  if (n != a->n_cols || n < 8 || n >= (int64_t{1} << 31)) return void(p.why = "shape");
+  if (n < 8 || nc >= (int64_t{1} << 31) || goff < 0 || goff + n > nc) return void(p.why = "shape");
   if (a->nnz > 27 * n || a->nnz < 2 * n) return void(p.why = "row lengths");
   ensure_host_copy(a);
   const std::vector<int64_t>& rp = a->h_row_ptr;
@@ -77,7 +80,7 @@ void build_stencil_plan(adp_csr* a, StencilPlan& p) {
     if (rp[r + 1] - rp[r] > kmax) kmax = rp[r + 1] - rp[r], rmax = r;
   if (kmax != 27 && kmax != 7) return void(p.why = "longest row is not 7 or 27 entries");
   std::vector<int64_t> off(static_cast<size_t>(kmax));
-  for (int64_t k = 0; k < kmax; ++k) off[k] = static_cast<int64_t>(ci[rp[rmax] + k]) - rmax;
+  for (int64_t k = 0; k < kmax; ++k) off[k] = static_cast<int64_t>(ci[rp[rmax] + k]) - (rmax + goff);
   // runs of consecutive offsets and their centres
   std::vector<int64_t> centre, len;
   for (int64_t k = 0; k < kmax;) {
@@ -102,11 +105,13 @@ void build_stencil_plan(adp_csr* a, StencilPlan& p) {
   const int64_t h = static_cast<int64_t>(centre.size()) / 2;
   for (int64_t j = 0; j <= h; ++j)
     if (centre[h - j] != -centre[h + j]) return void(p.why = "offsets not symmetric");
-  if (sy < 3 || sz <= sy || sz % sy != 0 || n % sz != 0) return void(p.why = "no grid strides");
+  if (sy < 3 || sz <= sy || sz % sy != 0 || nc % sz != 0 || n % sz != 0 || goff % sz != 0)
+    return void(p.why = "no grid strides (or rows / offset not whole planes)");
   p.nx = sy;
   p.ny = sz / sy;
-  p.nz = n / sz;
-  if (p.ny < 3 || p.nz < 3) return void(p.why = "grid too thin");
+  p.nz = n / sz;    // planes of the operator's rows
+  p.nzw = nc / sz;  // planes of the (extended) grid its columns index
+  if (p.ny < 3) return void(p.why = "grid too thin");
   p.kind = static_cast<int>(kmax);
   // the offset set in ascending column order: (dz, dy, dx) lexicographic
   std::vector<Off> set;
@@ -122,19 +127,20 @@ void build_stencil_plan(adp_csr* a, StencilPlan& p) {
   std::vector<double> diag(static_cast<size_t>(p.nz * p.ny * p.nxp), 0.0);
   bool have[27] = {};
   for (int64_t r = 0; r < n; ++r) {
-    const int64_t x = r % p.nx, y = (r / p.nx) % p.ny, z = r / sz;
+    const int64_t g = r + goff;
+    const int64_t x = g % p.nx, y = (g / p.nx) % p.ny, z = g / sz;
     int64_t e = rp[r];
     const int64_t e1 = rp[r + 1];
     for (const Off& o : set) {
-      if (x + o.dx < 0 || x + o.dx >= p.nx || y + o.dy < 0 || y + o.dy >= p.ny || z + o.dz < 0 || z + o.dz >= p.nz)
+      if (x + o.dx < 0 || x + o.dx >= p.nx || y + o.dy < 0 || y + o.dy >= p.ny || z + o.dz < 0 || z + o.dz >= p.nzw)
         continue;
-      const int64_t c = r + o.dx + sy * o.dy + sz * o.dz;
+      const int64_t c = g + o.dx + sy * o.dy + sz * o.dz;
       if (e >= e1 || ci[e] != c) return void(p.why = "row " + std::to_string(r) + ": pattern");
       const double v = val[e];
       if (!std::isfinite(v)) return void(p.why = "non-finite value");
       const int idx = (o.dz + 1) * 9 + (o.dy + 1) * 3 + (o.dx + 1);
       if (idx == 13) {
-        diag[static_cast<size_t>((z * p.ny + y) * p.nxp + x)] = v;
+        diag[static_cast<size_t>(((r / sz) * p.ny + y) * p.nxp + x)] = v;
       } else if (!have[idx]) {
         p.w[idx] = v;
         have[idx] = true;
@@ -231,10 +237,19 @@ struct Geo {
 struct SwArgs {
   char* out;
   uint64_t ldo_b;
-  int32_t nx, ny, nz, q;
+  int32_t nx, ny, q;
+  int32_t nzo;       // output planes of the launch
+  int32_t zv0;       // V / Y / out / diagonal plane of output plane 0 (row_begin / plane)
+  int32_t zw0;       // W plane of output plane 0 ((row_begin + goff) / plane)
+  int32_t wlo, whi;  // W planes the launch reads: [zw0 - 1, zw0 + nzo] inside the tensor
+  int32_t nzv;       // planes of the V / Y / diagonal tensors
   int32_t tiles_x, tiles_y, n_items;
   double s0, s1, s2;
   double w[27];  // constant values by offset; read as constant-bank operands of the DMULs
+  // peer-memory halo (multi-GPU row partition): output rows r in [lo, hi) are also stored to
+  // dst + (r + shift) * ld_b, a neighbour's halo rows mapped over NVLink (see cheb_lean.cu)
+  PushTarget push[kMaxPush];
+  int32_t n_push;
 };
 
 template <int NW, int KIND>
@@ -266,7 +281,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int tiles = p.tiles_x * p.tiles_y;
 
-  if (warp == NW) {  // producer
+  if (warp == NW) {  // producer: per W plane its halo tile + the centre values of that plane's outputs,
+                     // then the V / Y tiles of that output plane (consumed one plane later)
     if (lane == 0) {
       const uint64_t pol = policy_evict_first(1.0f);
       uint32_t sw = 0, pw = 1, sv = 0, pv = 1;  // a fresh empty barrier's preceding phase counts as done
@@ -274,19 +290,22 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         const int panel = item / tiles, t = item - panel * tiles;
         const int ty = t / p.tiles_x, tx = t - ty * p.tiles_x;
         const int x0 = tx * kTX, y0 = ty * NW, c0 = panel * kPW;
-        for (int z = 0; z < p.nz; ++z) {
+        for (int wz = p.wlo; wz <= p.whi; ++wz) {
+          const int o = wz - p.zw0;  // the output plane whose own W plane this is
           mbar_wait(empty_w + sw, pw);
           uint8_t* ws = smem + sw * G::kWS;
           mbar_expect_tx(full_w + sw, G::kW + G::kD);
-          tma4d(ws, &tm_w, c0, x0 - 1, y0 - 1, z, full_w + sw);
-          tma3d(ws + G::kW, &tm_d, x0, y0, z, full_w + sw);
+          tma4d(ws, &tm_w, c0, x0 - 1, y0 - 1, wz, full_w + sw);
+          tma3d(ws + G::kW, &tm_d, x0, y0, min(max(p.zv0 + o, 0), p.nzv - 1), full_w + sw);  // unused unless o is an output
           if (++sw == kSW) sw = 0, pw ^= 1;
-          mbar_wait(empty_v + sv, pv);
-          uint8_t* vs = smem + kSW * G::kWS + sv * G::kVS;
-          mbar_expect_tx(full_v + sv, G::kVS);
-          tma4d_hint(vs, &tm_v, c0, x0, y0, z, full_v + sv, pol);
-          tma4d_hint(vs + G::kT, &tm_y, c0, x0, y0, z, full_v + sv, pol);
-          if (++sv == kSV) sv = 0, pv ^= 1;
+          if (o >= 0 && o < p.nzo) {
+            mbar_wait(empty_v + sv, pv);
+            uint8_t* vs = smem + kSW * G::kWS + sv * G::kVS;
+            mbar_expect_tx(full_v + sv, G::kVS);
+            tma4d_hint(vs, &tm_v, c0, x0, y0, p.zv0 + o, full_v + sv, pol);
+            tma4d_hint(vs + G::kT, &tm_y, c0, x0, y0, p.zv0 + o, full_v + sv, pol);
+            if (++sv == kSV) sv = 0, pv ^= 1;
+          }
         }
       }
     }
@@ -297,6 +316,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
   const int yl = warp;
   const uint64_t pol = policy_evict_first(1.0f);
   uint32_t sw = 0, pw = 0, sv = 0, pv = 0, sprev = 0;
+  bool have_prev = false;
   double A0[kTX], A1[kTX], A2[kTX];
 #pragma unroll
   for (int x = 0; x < kTX; ++x) A0[x] = A1[x] = A2[x] = 0.0;
@@ -308,9 +328,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
     const bool live = y < p.ny && c < p.q;
     char* obase = p.out + static_cast<uint64_t>(c) * 8;
 
-    // one plane step: plane z's products into lo (plane z-1), mid (z), hi (z+1); then plane z-1's epilogue
-    auto step = [&](int z, double(&lo)[kTX], double(&mid)[kTX], double(&hi)[kTX]) {
-      if (z < p.nz) {
+    // one step per W plane wz (and one after the last): plane wz's products into lo (the output whose own
+    // plane is wz - 1), mid (wz), hi (wz + 1); then lo's epilogue if it is an output plane of the launch
+    auto step = [&](int wz, double(&lo)[kTX], double(&mid)[kTX], double(&hi)[kTX]) {
+      const bool real = wz <= p.whi;
+      if (real) {
         mbar_wait(full_w + sw, pw);
         const double* ws = reinterpret_cast<const double*>(smem + sw * G::kWS);
         const double* ds = reinterpret_cast<const double*>(smem + sw * G::kWS + G::kW) + yl * kTX;
@@ -326,9 +348,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx) {
                 const double wv = w[x + dx];
-                hi[x] = mac(hi[x], p.w[dy * 3 + dx], wv);  // dz = -1 entries of plane z+1
+                hi[x] = mac(hi[x], p.w[dy * 3 + dx], wv);  // dz = -1 entries of plane wz+1
                 mid[x] = mac(mid[x], (dy == 1 && dx == 1) ? ds[x] : p.w[9 + dy * 3 + dx], wv);
-                lo[x] = mac(lo[x], p.w[18 + dy * 3 + dx], wv);  // dz = +1 entries of plane z-1
+                lo[x] = mac(lo[x], p.w[18 + dy * 3 + dx], wv);  // dz = +1 entries of plane wz-1
               }
             }
           }
@@ -351,51 +373,62 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
           }
         }
       }
-      if (z >= 1) {  // plane z-1 complete: v = (((s0 aw) + (s1 w)) - v) + (s2 y)  (cheb_filter.cpp:170-171,176-177)
+      const int o = wz - p.zw0 - 1;
+      if (o >= 0 && o < p.nzo) {  // complete: v = (((s0 aw) + (s1 w)) - v) + (s2 y)  (cheb_filter.cpp:170-171,176-177)
         mbar_wait(full_v + sv, pv);
         const double* own = reinterpret_cast<const double*>(smem + sprev * G::kWS) + ((yl + 1) * G::WX + 1) * kPW + lane;
         const double* vs = reinterpret_cast<const double*>(smem + kSW * G::kWS + sv * G::kVS) + yl * kTX * kPW + lane;
         const double* ys = vs + kTX * NW * kPW;
         if (live) {
-          char* ob = obase + (static_cast<uint64_t>(z - 1) * p.ny + y) * p.nx * p.ldo_b;
+          const int64_t rrow = (static_cast<int64_t>(p.zv0 + o) * p.ny + y) * p.nx + x0;  // operator row of x = 0
+          char* ob = obase + static_cast<uint64_t>(rrow) * p.ldo_b;
 #pragma unroll
           for (int x = 0; x < kTX; ++x) {
             if (x0 + x < p.nx) {
               const double res =
                   __dadd_rn(__dsub_rn(__dadd_rn(__dmul_rn(p.s0, lo[x]), __dmul_rn(p.s1, own[x * kPW])), vs[x * kPW]),
                             __dmul_rn(p.s2, ys[x * kPW]));
-              st_hint(ob + static_cast<uint64_t>(x0 + x) * p.ldo_b, res, pol);
+              st_hint(ob + static_cast<uint64_t>(x) * p.ldo_b, res, pol);
+              for (int tgt = 0; tgt < p.n_push; ++tgt) {  // uniform: one plane's rows are all in or all out
+                const int64_t r = rrow + x;
+                if (r >= p.push[tgt].lo && r < p.push[tgt].hi)
+                  *reinterpret_cast<double*>(p.push[tgt].dst + static_cast<uint64_t>(r + p.push[tgt].shift) *
+                                                                   p.push[tgt].ld_b + static_cast<uint64_t>(c) * 8) = res;
+              }
             }
           }
         }
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(empty_v + sv);
-          mbar_arrive(empty_w + sprev);
-        }
+        if (lane == 0) mbar_arrive(empty_v + sv);
         if (++sv == kSV) sv = 0, pv ^= 1;
       }
+      if (have_prev) {  // plane wz - 1 is read for the last time (own rows of lo's epilogue)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_w + sprev);
+      }
 #pragma unroll
-      for (int x = 0; x < kTX; ++x) lo[x] = 0.0;  // becomes plane z+2's accumulator
-      if (z < p.nz) {
+      for (int x = 0; x < kTX; ++x) lo[x] = 0.0;  // becomes plane wz+2's accumulator
+      have_prev = real;
+      if (real) {
         sprev = sw;
         if (++sw == kSW) sw = 0, pw ^= 1;
       }
     };
 
-    for (int z = 0;;) {
-      step(z, A2, A0, A1);
-      if (++z > p.nz) break;
-      step(z, A0, A1, A2);
-      if (++z > p.nz) break;
-      step(z, A1, A2, A0);
-      if (++z > p.nz) break;
+    for (int wz = p.wlo;;) {
+      step(wz, A2, A0, A1);
+      if (++wz > p.whi + 1) break;
+      step(wz, A0, A1, A2);
+      if (++wz > p.whi + 1) break;
+      step(wz, A1, A2, A0);
+      if (++wz > p.whi + 1) break;
     }
-    // the roles rotate with z; the next item starts again with (A2, A0, A1), all zero (the
-    // accumulator of the nonexistent plane nz holds plane nz-1's dz = -1 products: cleared)
+    // the roles rotate with wz; the next item starts again with (A2, A0, A1), all zero (accumulators of
+    // planes past the launch's outputs hold products that no output takes: cleared)
 #pragma unroll
     for (int x = 0; x < kTX; ++x) A0[x] = A1[x] = A2[x] = 0.0;
   }
+  if (p.n_push) __threadfence_system();  // the peer stores are performed before the signal kernel that follows
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -423,10 +456,10 @@ CUtensorMap make_map(int rank, const void* base, const cuuint64_t* dims, const c
   return m;
 }
 
-// A row-major n x q block (row pitch ld_b bytes) seen as [nz][ny][nx][q].
-CUtensorMap block_map(const void* base, const StencilPlan& sp, int64_t q, int64_t ld_b, int bx, int by) {
+// A row-major block (row pitch ld_b bytes) of `planes` grid planes seen as [planes][ny][nx][q].
+CUtensorMap block_map(const void* base, const StencilPlan& sp, int64_t planes, int64_t q, int64_t ld_b, int bx, int by) {
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(q), static_cast<cuuint64_t>(sp.nx),
-                              static_cast<cuuint64_t>(sp.ny), static_cast<cuuint64_t>(sp.nz)};
+                              static_cast<cuuint64_t>(sp.ny), static_cast<cuuint64_t>(planes)};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld_b), static_cast<cuuint64_t>(ld_b * sp.nx),
                                  static_cast<cuuint64_t>(ld_b * sp.nx * sp.ny)};
   const cuuint32_t box[4] = {kPW, static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), 1};
@@ -436,13 +469,19 @@ CUtensorMap block_map(const void* base, const StencilPlan& sp, int64_t q, int64_
 template <int NW, int KIND>
 void launch_sweep(adp_ctx* ctx, const StepArgs& s, const StencilPlan& sp) {
   using G = Geo<NW>;
+  const int64_t plane = sp.nx * sp.ny;
   SwArgs k{};
   k.out = static_cast<char*>(s.out);
   k.ldo_b = static_cast<uint64_t>(s.ld_out) * 8;
   k.nx = static_cast<int32_t>(sp.nx);
   k.ny = static_cast<int32_t>(sp.ny);
-  k.nz = static_cast<int32_t>(sp.nz);
   k.q = static_cast<int32_t>(s.q);
+  k.nzo = static_cast<int32_t>((s.row_end - s.row_begin) / plane);
+  k.zv0 = static_cast<int32_t>(s.row_begin / plane);
+  k.zw0 = static_cast<int32_t>((s.row_begin + sp.goff) / plane);
+  k.wlo = std::max(k.zw0 - 1, 0);
+  k.whi = static_cast<int32_t>(std::min<int64_t>(k.zw0 + k.nzo, sp.nzw - 1));
+  k.nzv = static_cast<int32_t>(sp.nz);
   k.tiles_x = static_cast<int32_t>((sp.nx + kTX - 1) / kTX);
   k.tiles_y = static_cast<int32_t>((sp.ny + NW - 1) / NW);
   const int64_t panels = (s.q + kPW - 1) / kPW;
@@ -451,9 +490,11 @@ void launch_sweep(adp_ctx* ctx, const StepArgs& s, const StencilPlan& sp) {
   k.s1 = s.s1;
   k.s2 = s.s2;
   for (int i = 0; i < 27; ++i) k.w[i] = sp.w[i];
-  const CUtensorMap tm_w = block_map(s.gsrc, sp, s.q, s.ld * 8, kTX + 2, NW + 2);
-  const CUtensorMap tm_v = block_map(s.vin, sp, s.q, s.ld * 8, kTX, NW);
-  const CUtensorMap tm_y = block_map(s.yin, sp, s.q, s.ld_y * 8, kTX, NW);
+  k.n_push = s.n_push;
+  for (int t = 0; t < s.n_push; ++t) k.push[t] = s.push[t];
+  const CUtensorMap tm_w = block_map(s.gsrc, sp, sp.nzw, s.q, s.ld * 8, kTX + 2, NW + 2);
+  const CUtensorMap tm_v = block_map(s.vin, sp, sp.nz, s.q, s.ld * 8, kTX, NW);
+  const CUtensorMap tm_y = block_map(s.yin, sp, sp.nz, s.q, s.ld_y * 8, kTX, NW);
   const cuuint64_t ddims[3] = {static_cast<cuuint64_t>(sp.nx), static_cast<cuuint64_t>(sp.ny),
                                static_cast<cuuint64_t>(sp.nz)};
   const cuuint64_t dstr[2] = {static_cast<cuuint64_t>(sp.nxp * 8), static_cast<cuuint64_t>(sp.nxp * sp.ny * 8)};
@@ -470,10 +511,10 @@ void launch_sweep(adp_ctx* ctx, const StepArgs& s, const StencilPlan& sp) {
 
 }  // namespace
 
-const StencilPlan* get_stencil_plan(adp_csr* a) {
-  if (!a->stencil) {
+const StencilPlan* get_stencil_plan(adp_csr* a, int64_t goff) {
+  if (!a->stencil || a->stencil->goff != goff) {
     auto p = std::make_unique<StencilPlan>();
-    build_stencil_plan(a, *p);
+    build_stencil_plan(a, goff, *p);
     a->stencil = std::move(p);
   }
   return a->stencil.get();
@@ -483,11 +524,12 @@ bool launch_step_sweep(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
   if (mode != StepMode::Step || a->dtype != ADP_F64) return false;
   if (ctx->variant == 0 && !ctx->auto_sweep) return false;
-  if (s.row_begin != 0 || s.row_end != a->n_rows || s.goff != 0 || s.n_push != 0) return false;
-  if (a->n_rows != a->n_cols || a->nnz > 27 * a->n_rows || a->nnz < 2 * a->n_rows) return false;
+  if (a->nnz > 27 * a->n_rows || a->nnz < 2 * a->n_rows || s.row_end <= s.row_begin) return false;
   if (s.q < 1 || s.q >= (int64_t{1} << 31) || s.ld % 2 || s.ld_y % 2) return false;
-  const StencilPlan* sp = get_stencil_plan(const_cast<adp_csr*>(a));
+  const StencilPlan* sp = get_stencil_plan(const_cast<adp_csr*>(a), s.goff);
   if (!sp->valid) return false;
+  const int64_t plane = sp->nx * sp->ny;
+  if (s.row_begin % plane || s.row_end % plane) return false;  // whole grid planes only
   if (sp->kind == 27) launch_sweep<8, 27>(ctx, s, *sp);
   else launch_sweep<8, 7>(ctx, s, *sp);
   return true;

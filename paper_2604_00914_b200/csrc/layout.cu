@@ -299,6 +299,7 @@ __global__ void halo_signal_kernel(CounterSet cs, uint64_t value) {
 }
 
 __global__ void halo_wait_kernel(CounterSet cs, uint64_t expected, uint64_t timeout_ns, int* failed) {
+  if (*(volatile int*)failed) return;  // an earlier wait of this call timed out: fail fast, do not spin again
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int i = 0; i < cs.n; ++i) {
@@ -359,7 +360,10 @@ void launch_halo_wait(adp_ctx* ctx, const uint64_t* const* counters, int32_t n, 
   CounterSet cs{};
   cs.n = n;
   for (int i = 0; i < n; ++i) cs.c[i] = const_cast<uint64_t*>(counters[i]);
-  if (!ctx->halo_failed) ADP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->halo_failed), sizeof(int)));
+  if (!ctx->halo_failed) {  // fresh memory may hold stale bytes: clear before the first wait reads it
+    ADP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->halo_failed), sizeof(int)));
+    ADP_CUDA(cudaMemsetAsync(ctx->halo_failed, 0, sizeof(int), ctx->stream));
+  }
   halo_wait_kernel<<<1, 1, 0, ctx->stream>>>(cs, expected, static_cast<uint64_t>(timeout_ms) * 1000000ull,
                                              ctx->halo_failed);
   ADP_LAUNCH_CHECK();

@@ -594,6 +594,14 @@ adp_status adp_solve_result_destroy(adp_solve_result* r) {
   return guarded([&] { delete r; });
 }
 
+adp_status adp_spmv_device(adp_ctx* ctx, const adp_csr* a, const double* x, double* y) {
+  return guarded([&] {
+    ADP_CUDA(cudaSetDevice(ctx->device));
+    adp::spmv(ctx, a, x, y);
+    ADP_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 adp_status adp_lanczos_bounds(adp_ctx* ctx, const adp_csr* a, int32_t steps, uint64_t seed, double* lambda_min,
                               double* lambda_max, int64_t* spmv_count) {
   return guarded([&] { adp::spectrum_bounds(ctx, a, steps, seed, lambda_min, lambda_max, spmv_count); });

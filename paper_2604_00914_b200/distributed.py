@@ -127,6 +127,7 @@ class DistributedFilter:
         self.world, self.rank = world, rank
         self.ranges = ranges or partition_rows(a_global, world)
         self.part = local_part(a_global, self.ranges, rank)
+        self.cplx = bool(a_global.is_complex)  # blocks are complex128 for a complex operator
         bounds = []
         for k in range(world):
             p0, p1 = self.ranges[k]
@@ -164,6 +165,18 @@ class DistributedFilter:
             if hi > lo:
                 be.step(self.op, part, mode, g, vin, yin, out, wout, (lo, hi), *s)
 
+    def spmm(self, x_local):
+        """My rows of A X (maspmm, tiled_matrix.hpp:184-210): X's halo rows exchanged, then the Spmm
+        mode of the step kernel (the sharded solve's Rayleigh-Ritz, residuals and Lanczos)."""
+        be, part = self.backend, self.part
+        q = be.width(x_local)
+        ext = be.alloc(part.n_ext, q, self.cplx)
+        g0, g1 = part.goff, part.goff + part.n_local
+        be.copy_rows(be.rows(ext, g0, g1), x_local)
+        out = be.alloc(part.n_local, q, self.cplx)
+        self._run(SPMM, ext, None, None, out, None, (0.0, 0.0, 0.0, 0.0))
+        return out
+
     def apply(self, coeffs, l1, l2, x_local, degree: int):
         """x_local: my n_local x q rows (backend block). Returns my rows of rho(l(A)) X."""
         be, part = self.backend, self.part
@@ -174,15 +187,15 @@ class DistributedFilter:
         if deg == 0:
             return be.scale(x_local, float(coeffs[0]))
         n_ext = part.n_ext
-        a_buf, b_buf = be.alloc(n_ext, q), be.alloc(n_ext, q)
+        a_buf, b_buf = be.alloc(n_ext, q, self.cplx), be.alloc(n_ext, q, self.cplx)
         g0, g1 = part.goff, part.goff + part.n_local
         if deg == 1:
             be.copy_rows(be.rows(a_buf, g0, g1), x_local)
-            out = be.alloc(part.n_local, q)
+            out = be.alloc(part.n_local, q, self.cplx)
             self._run(DEG1, a_buf, None, None, out, None, (coeffs[0], coeffs[1], l1, l2))
             return out
         # the First step gathers Y: Y needs its halo too, so stage it in an extended buffer
-        y_ext = be.alloc(n_ext, q)
+        y_ext = be.alloc(n_ext, q, self.cplx)
         be.copy_rows(be.rows(y_ext, g0, g1), x_local)
         # w = c_d y -> a_buf ; v -> b_buf
         self._run(FIRST, y_ext, None, None, be.rows(b_buf, g0, g1), be.rows(a_buf, g0, g1),
@@ -192,7 +205,7 @@ class DistributedFilter:
             v_rows = be.rows(cur_v, g0, g1)
             self._run(STEP, cur_w, v_rows, x_local, v_rows, None, (2.0 * l1, 2.0 * l2, coeffs[j], 0.0))
             cur_w, cur_v = cur_v, cur_w
-        out = be.alloc(part.n_local, q)
+        out = be.alloc(part.n_local, q, self.cplx)
         self._run(STEP, cur_w, be.rows(cur_v, g0, g1), x_local, out, None, (l1, l2, coeffs[0], 0.0))
         return out
 
@@ -213,7 +226,9 @@ class CudaStepBackend:
 
         return DeviceCsr(part.csr, self.ctx)
 
-    def alloc(self, n, q):
+    def alloc(self, n, q, cplx=False):
+        if cplx:  # complex128: 16-byte elements, any width is 16-byte aligned
+            return self.torch.zeros(n, q, dtype=self.torch.complex128, device="cuda")
         ld = ((q + 1) // 2) * 2
         return self.torch.zeros(n, ld, dtype=self.torch.float64, device="cuda")[:, :q]
 
@@ -445,7 +460,7 @@ class PeerHaloFilter(DistributedFilter):
         if self.q == q:
             return
         be, part = self.backend, self.part
-        self.bufs = {name: be.alloc(part.n_ext, q) for name in ("y", "a", "b")}
+        self.bufs = {name: be.alloc(part.n_ext, q, self.cplx) for name in ("y", "a", "b")}
         self.counters = be.new_counters(self.world)
         items = {f"buf_{k}": be.base(v) for k, v in self.bufs.items()}
         items["counters"] = self.counters
@@ -520,7 +535,7 @@ class PeerHaloFilter(DistributedFilter):
             be.copy_rows(be.rows(a_buf, g0, g1), x_local)
             self._push_input(x_local, "a")
             yield
-            out = be.alloc(part.n_local, q)
+            out = be.alloc(part.n_local, q, self.cplx)
             self._run_fused(DEG1, a_buf, None, None, out, None, (coeffs[0], coeffs[1], l1, l2), None)
             be.check()
             return out
@@ -537,7 +552,7 @@ class PeerHaloFilter(DistributedFilter):
             self._run_fused(STEP, cur_w, v_rows, x_local, v_rows, None, (2.0 * l1, 2.0 * l2, coeffs[j], 0.0), names[1])
             yield
             cur_w, cur_v, names = cur_v, cur_w, (names[1], names[0])
-        out = be.alloc(part.n_local, q)
+        out = be.alloc(part.n_local, q, self.cplx)
         self._run_fused(STEP, cur_w, be.rows(cur_v, g0, g1), x_local, out, None, (l1, l2, coeffs[0], 0.0), None)
         be.check()
         return out

@@ -1,29 +1,21 @@
-"""Eigenpairs of complex Hermitian operators (configs 3 and 5) through the real embedding.
+"""Eigenpairs of complex Hermitian operators (configs 3 and 5), natively in complex128 on the device.
 
 The reference solver is real symmetric only (``solve`` in proj/src/solver.cpp:119-360
-takes a CsrMatrixd). For H = A + iB Hermitian, the real symmetric
+takes a CsrMatrixd). ``solve_hermitian`` runs the same filtered subspace iteration on H itself
+(sharded.ShardedSolver with complex128 blocks on one GPU): the complex fused filter kernel, complex
+SpMM, Gram matrices X^H X and projections Q^H A Q through cuBLAS zgemm / zherk-class products,
+Cholesky (zpotrf) and the Hermitian eigensolver (zheevd) through cuSOLVER, residuals on H. No host
+numpy arithmetic and no real 2n embedding in the product path.
 
-    S = [[A, -B],
-         [B,  A]]          (2n x 2n)
-
-satisfies S [x; y] = lambda [x; y]  <=>  H (x + iy) = lambda (x + iy): every eigenvalue of H is an
-eigenvalue of S with twice its multiplicity, and every eigenvector of S maps to one of H. This is the
-same embedding that pins the complex filter to the real (reference-exact) one.
-
-``solve_hermitian`` runs the GPU ``solve`` on S (the window [a, b] unchanged; the subspace size follows
-the reference rule on S's doubled count, or twice ``p_override``), maps the converged S eigenvectors to
-C^n, extracts an orthonormal basis of their span (each eigenvector of H arrives twice, as v and i v),
-and finishes with one Rayleigh-Ritz step on H itself (the complex SpMM on the device), so the returned
-eigenpairs are H's, with their residuals measured on H.
+``hermitian_embedding`` (the real 2n x 2n S = [[A, -B], [B, A]] of H = A + iB, whose spectrum is H's
+with doubled multiplicity) stays as a TEST PIN: it ties the complex path to the real, reference-exact
+one (tests/test_oracle_pins.py, tests/test_gpu_solver.py).
 """
 from __future__ import annotations
 
-import dataclasses
-
 import numpy as np
 
-from .operator import Context, DeviceCsr, maspmm
-from .solver import SolveResult, SolverConfig, solve
+from .solver import SolveResult, SolverConfig
 from .sparse import CsrMatrix
 
 
@@ -49,35 +41,30 @@ def hermitian_embedding(h: CsrMatrix) -> CsrMatrix:
     return CsrMatrix.from_triplets(2 * n, 2 * n, r[keep], c[keep], x[keep])
 
 
-def solve_hermitian(h: CsrMatrix, config: SolverConfig, ctx: Context | None = None) -> SolveResult:
-    """Interior eigenpairs of a complex Hermitian CSR matrix in [interval_a, interval_b] (GPU)."""
+def solve_hermitian(h, config: SolverConfig, ctx=None, vectors_to_host: bool = True) -> SolveResult:
+    """Interior eigenpairs of a complex Hermitian operator in [interval_a, interval_b] on this process's
+    GPU (torch's current device unless ``ctx`` is given). ``h``: a host CsrMatrix or a complex DeviceCsr
+    (config 5's operator is generated on the device and never exists on the host)."""
+    import torch
+
+    from .operator import DeviceCsr, default_context
+    from .sharded import DeviceSparse, LocalComm, ShardedSolver, TorchOps
+
     if not h.is_complex:
         raise ValueError("solve_hermitian: complex operator expected (use solve for real symmetric ones)")
-    n = h.n_rows
-    ctx = ctx or Context(0)
-    ds = DeviceCsr(hermitian_embedding(h), ctx)
-    cfg = dataclasses.replace(config, p_override=2 * config.p_override if config.p_override else None)
-    r = solve(ds, cfg)
-    ds.close()
-    z = r.eigenvectors
-    if z.shape[1] == 0:
-        return dataclasses.replace(r, eigenvectors=np.zeros((n, 0), np.complex128))
-    v = z[:n] + 1j * z[n:]
-    # orthonormal basis of span(v): the Gram matrix of (v, i v) pairs has eigenvalues 2 and 0
-    g = v.conj().T @ v
-    d, w = np.linalg.eigh((g + g.conj().T) / 2)
-    keep = d > 0.25 * float(d.max())
-    u = v @ (w[:, keep] / np.sqrt(d[keep]))
-    # one Rayleigh-Ritz step on H (complex SpMM on the device)
-    dh = DeviceCsr(h, ctx)
-    hu = maspmm(dh, u)
-    t = u.conj().T @ hu
-    theta, y = np.linalg.eigh((t + t.conj().T) / 2)
-    vecs = u @ y
-    hv = hu @ y
-    res = np.linalg.norm(hv - vecs * theta, axis=0)
-    dh.close()
-    inside = (theta >= config.interval_a) & (theta <= config.interval_b)
-    theta, vecs, res = theta[inside], vecs[:, inside], res[inside]
-    return dataclasses.replace(r, eigenvalues=theta, eigenvectors=vecs,
-                               max_residual=float(res.max()) if len(res) else 0.0)
+    if h.n_rows != h.n_cols:
+        raise ValueError("solve_hermitian: square operators only")
+    if isinstance(h, DeviceCsr):
+        da, own = h, False
+    else:
+        ctx = ctx or default_context(torch.cuda.current_device())
+        da, own = DeviceCsr(h, ctx), True
+    try:
+        ops = TorchOps(True, torch.device("cuda", da.ctx.device))
+        r = ShardedSolver(h.n_rows, True, ops, DeviceSparse(da), LocalComm()).solve(config)
+    finally:
+        if own:
+            da.close()
+    if vectors_to_host:
+        r.eigenvectors = r.eigenvectors.cpu().numpy() if hasattr(r.eigenvectors, "cpu") else r.eigenvectors
+    return r

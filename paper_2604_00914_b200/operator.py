@@ -229,6 +229,19 @@ def maspmm(a: DeviceCsr, b: np.ndarray, c: np.ndarray | None = None, accumulate:
     return c
 
 
+def csr_spmv_device(a: DeviceCsr, x, y):
+    """y = A x (csr_matrix.hpp:122-134: sequential CSR-order accumulation) on torch CUDA fp64 vectors."""
+    import torch
+
+    if a.is_complex:
+        raise ConfigError("csr_spmv: real operators only")
+    if x.numel() != a.n_cols or y.numel() != a.n_rows or not (x.is_contiguous() and y.is_contiguous()):
+        raise DimensionError("csr_spmv: vector sizes do not match the operator")
+    a.ctx.set_stream(torch.cuda.current_stream(x.device))
+    check(lib().adp_spmv_device(a.ctx.h, a.h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr())))
+    return y
+
+
 def maspmm_device(a: DeviceCsr, b, c, accumulate: bool = False):
     """C (+)= A B on torch CUDA tensors (row-major), queued on the current stream."""
     import torch

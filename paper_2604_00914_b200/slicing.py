@@ -100,8 +100,9 @@ def solve_sliced(dev_csr, config, n_slices: int | None = None, slices=None, grou
                  overlap: float = 0.01, rtol: float = 1e-8) -> SlicedResult:
     """Solve config.interval_a..interval_b slice by slice and merge (see the module docstring).
 
-    ``solve_fn(dev_csr, cfg) -> SolveResult`` defaults to the GPU `solve` (to `solve_hermitian` when
-    ``dev_csr`` is a complex host CsrMatrix: config 5's slices); tests inject a stand-in.
+    ``solve_fn(dev_csr, cfg) -> SolveResult`` defaults to the GPU `solve` (to the native complex
+    `solve_hermitian` when ``dev_csr`` is complex -- a host CsrMatrix or a device-generated DeviceCsr:
+    config 5's slices); tests inject a stand-in.
     Pairs found by two neighbouring slices inside their overlap (values within rtol x scale) are
     kept once; genuinely repeated eigenvalues are matched one to one, so multiplicities survive.
     """
@@ -111,12 +112,10 @@ def solve_sliced(dev_csr, config, n_slices: int | None = None, slices=None, grou
     from .solver import solve
 
     if solve_fn is None:
-        from .sparse import CsrMatrix
-
-        if isinstance(dev_csr, CsrMatrix) and dev_csr.is_complex:
+        if getattr(dev_csr, "is_complex", False):  # host CsrMatrix or device-generated DeviceCsr (config 5)
             from .hermitian import solve_hermitian
 
-            solve_fn = solve_hermitian
+            solve_fn = solve_hermitian  # native complex128 solve on this rank's current GPU
         else:
             solve_fn = solve
     a, b = float(config.interval_a), float(config.interval_b)

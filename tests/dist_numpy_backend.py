@@ -29,8 +29,8 @@ class NumpyStepBackend:
     def upload(self, part):
         return part.csr
 
-    def alloc(self, n, q):
-        return np.zeros((n, q))
+    def alloc(self, n, q, cplx=False):
+        return np.zeros((n, q), np.complex128 if cplx else np.float64)
 
     def width(self, x):
         return x.shape[1]
@@ -50,7 +50,7 @@ class NumpyStepBackend:
         nr = hi - lo
         counts = np.diff(rp[lo:hi + 1])
         kmax = int(counts.max()) if nr else 0
-        acc = np.zeros((nr, g.shape[1]))
+        acc = np.zeros((nr, g.shape[1]), g.dtype)
         for k in range(kmax):
             m = counts > k
             idx = rp[lo:hi][m] + k

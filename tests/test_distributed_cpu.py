@@ -181,3 +181,41 @@ def test_peer_halo_boundary_covers_sends_and_halo_reads():
             for lo, hi in p.sends.values():
                 assert hi - p.r0 <= i0 or lo - p.r0 >= i1
             assert set(pf.neighbours) == set(p.sends) | set(p.recvs)
+
+
+# A complex Hermitian operator (config 3's structure) through the peer-halo filter: blocks must be
+# complex128 end to end (DistributedFilter.cplx -> backend.alloc). The numpy backend's complex
+# arithmetic is its own, so the partitioned result is compared bitwise with the same backend on ONE
+# rank (the partition never changes an output element's arithmetic).
+@pytest.mark.parametrize("world,degree,q", [(2, 9, 3), (3, 4, 2)])
+def test_peer_halo_filter_threads_complex(orc, world, degree, q):
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    sys.path.insert(0, ROOT)
+    from dist_numpy_backend import NumpyStepBackend
+    from paper_2604_00914_b200 import configs
+    from paper_2604_00914_b200.distributed import LocalPeerDirectory, PeerHaloFilter
+
+    a = configs.peierls_lattice(9)
+    n = a.n_rows
+    f = orc.build_filter(-0.4, 0.3, (-5.0, 5.0), max(degree, 1), 0.5)
+    rng = np.random.default_rng(world)
+    x = rng.standard_normal((n, q)) + 1j * rng.standard_normal((n, q))
+
+    def run(w):
+        directory = LocalPeerDirectory(threading.Barrier(w))
+        filters = [PeerHaloFilter(a, NumpyStepBackend(jitter=0.001, seed=k), k, w, directory, timeout_ms=60000)
+                   for k in range(w)]
+
+        def rank_main(k):
+            r0, r1 = filters[k].ranges[k]
+            return filters[k].apply(f.coeffs, f.l1, f.l2, np.ascontiguousarray(x[r0:r1]), degree)
+
+        with ThreadPoolExecutor(w) as ex:
+            return np.concatenate(list(ex.map(rank_main, range(w))))
+
+    one = run(1)
+    assert one.dtype == np.complex128 and np.abs(one.imag).max() > 0
+    assert np.array_equal(run(world), one)

@@ -116,23 +116,40 @@ def test_emulated_ranks_bitwise(orc, world, degree, q):
 # back to back, ragged and narrow widths (narrow ones push with the copy kernel).
 @pytest.mark.parametrize("world,degree,q,kind", [(2, 12, 64, "lap"), (3, 7, 6, "lap"), (2, 1, 130, "lap"),
                                                   (4, 20, 256, "lap"), (2, 9, 2, "lap"), (3, 5, 100, "27pt"),
-                                                  (2, 6, 256, "27pt")])  # interior rows: cube kernel, ranged plan
+                                                  (2, 6, 256, "27pt"),  # interior rows: cube kernel, ranged plan
+                                                  (2, 8, 5, "herm"), (3, 5, 64, "herm"),  # complex128 blocks
+                                                  # slabs of whole grid planes: the plane-sweep kernel on the
+                                                  # interior AND on the pushed boundary planes
+                                                  (2, 12, 64, "lap_planes"), (3, 9, 40, "27pt_planes"),
+                                                  (4, 6, 34, "27pt_planes")])
 def test_peer_halo_lockstep_bitwise(orc, world, degree, q, kind):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2604_00914_b200 import configs
     from paper_2604_00914_b200.distributed import CudaStepBackend, LocalPeerDirectory, PeerHaloFilter, run_lockstep
 
-    a = configs.laplacian7_potential(20, -2.0, 2.0, seed=1) if kind == "lap" else configs.dft_like_27pt(12, 4, 2)
+    ranges = None
+    if kind == "herm":  # config 3's structure: complex128 blocks through alloc, steps and pushes
+        a = configs.peierls_lattice(24)
+    else:
+        a = configs.laplacian7_potential(20, -2.0, 2.0, seed=1) if kind.startswith("lap") else configs.dft_like_27pt(12, 4, 2)
+    if kind.endswith("_planes"):
+        import bench
+
+        plane = 400 if kind.startswith("lap") else 144
+        ranges = bench.plane_ranges(a.n_rows, plane, world)
     n = a.n_rows
-    f = adp.build_filter(5.9, 6.1, (-2.0, 14.0), 40, 0.5)
+    f = adp.build_filter(5.9, 6.1, (-2.0, 14.0), 40, 0.5) if kind != "herm" else adp.build_filter(-0.3, 0.2, (-5.0, 5.0), 40, 0.5)
     ctx = adp.Context(0)
     ctx.set_stream(torch.cuda.current_stream())
     directory = LocalPeerDirectory()
-    filters = [PeerHaloFilter(a, CudaStepBackend(ctx), k, world, directory, timeout_ms=5000) for k in range(world)]
+    filters = [PeerHaloFilter(a, CudaStepBackend(ctx), k, world, directory, ranges=ranges, timeout_ms=5000)
+               for k in range(world)]
     launches0 = ctx.launch_count
     for seed in (3, 4):
         x = orc.fill_gaussian(n, q, seed, 0)
+        if kind == "herm":
+            x = x + 1j * orc.fill_gaussian(n, q, seed + 10, 0)
         want = adp.clenshaw_apply(f, adp.DeviceCsr(a, ctx), x, degree)
         xs = []
         for k in range(world):
@@ -141,6 +158,8 @@ def test_peer_halo_lockstep_bitwise(orc, world, degree, q, kind):
         outs = run_lockstep(filters, xs, f.coeffs, f.l1, f.l2, degree)
         got = np.concatenate([o.cpu().numpy() for o in outs])
         assert np.array_equal(got, want), seed
+        if ranges is not None:
+            assert ctx.last_step_kernel == 5
     assert ctx.launch_count > launches0
 
 

@@ -1,6 +1,7 @@
 """Sweep the fused-step kernel's tuning variants on one configuration (GPU).
 
-Prints ms per degree-step launch and effective GB/s for each variant, and
+Prints ms per Step launch (a degree-d call minus a degree-2 call, over d - 2) and
+effective GB/s for each variant, and
 checks that every variant's result is bitwise identical to variant 0's.
 Usage: python tools/tune_step.py [--config c2] [--degree 30] [--variants 0,1,2]
 """
@@ -53,13 +54,18 @@ def main():
         y = torch.empty_like(x)
         adp.clenshaw_apply_device(f, da, x, args.degree, out=y)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.reps):
-            adp.clenshaw_apply_device(f, da, x, args.degree, out=y)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.reps / args.degree
+        def timed(deg):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.reps):
+                adp.clenshaw_apply_device(f, da, x, deg, out=y)
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / args.reps
+
+        # per Step launch: a degree-2 call (First + one Step) subtracted from the degree-d call
+        t2 = timed(2)
+        ms = (timed(args.degree) - t2) / (args.degree - 2)
         same = None
         if ref is None:
             ref = y.clone()
