@@ -462,11 +462,6 @@ def run_ours(args):
     bytes_call = call_bytes(n, nnz, q, degree, es, rp)
     value = bytes_call / (ms_step * 1e-3) / 1e9
     b_step = step_bytes(n, nnz, q, es, rp)
-    # the dominant kernel's average launch: the call's Step launches (degree - 1 of them: First + Steps),
-    # isolated by timing degree-2 calls (First + one Step) on the same stream and subtracting
-    t2 = time_filter(adp, da, f, x, y, 2, 3, stream) if degree > 2 else None
-    launch_ms = (ms_step - t2) / (degree - 2) if t2 is not None else ms_step / max(degree, 1)
-    achieved = b_step / (launch_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -503,6 +498,11 @@ def run_ours(args):
                "d2h_bytes_per_step": n * q * 8, "ms_per_step": round(t_e2e * 1e3, 3), "matches_device_result": same,
                "api": "adp_filter_apply (C-ABI, host column-major, pinned)"}
         del xh, yh
+    # the dominant kernel's average launch: the call's Step launches (degree - 1 of them: First + Steps),
+    # isolated by timing degree-2 calls (First + one Step) on the same stream and subtracting
+    t2 = time_filter(adp, da, f, x, y, 2, 3, stream) if degree > 2 else None
+    launch_ms = (ms_step - t2) / (degree - 2) if t2 is not None else ms_step / max(degree, 1)
+    achieved = b_step / (launch_ms * 1e-3) / 1e9
     del x, y
     da.close()
     ctx.close()

@@ -127,6 +127,8 @@ struct StencilPlan {
   int64_t goff = 0;           // row r is point r + goff of that grid
   int64_t nxp = 0;            // x pitch of the diagonal array (even: 16-byte rows for TMA)
   double w[27] = {};          // value at offset (dx, dy, dz): index (dz+1)*9 + (dy+1)*3 + (dx+1); centre unused
+  bool classes = false;       // 27: weights depend only on m = |dx|+|dy|+|dz| (cls[m]); 7: all neighbours -1
+  double cls[4] = {};
   double* d_diag = nullptr;   // [nz][ny][nxp] centre values
   std::string why;            // why the operator is not such a stencil (diagnostics)
   ~StencilPlan();

@@ -369,7 +369,8 @@ void launch_step(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   if (s.n_push == 0 || s.row_end <= s.row_begin || s.q == 0) return launch_step_impl(ctx, mode, s);
   if (mode != StepMode::First && mode != StepMode::Step) fail(ADP_ERR_CONFIG, "halo push: First / Step modes only");
   if (s.n_push > kMaxPush) fail(ADP_ERR_CONFIG, "halo push: too many targets");
-  if ((ctx->variant == 0 || ctx->variant == 5) && launch_step_sweep(ctx, mode, s)) return void(ctx->last_kernel = 5);
+  if ((ctx->variant == 0 || ctx->variant == 5) && launch_step_sweep(ctx, mode, s))
+    return void(ctx->last_kernel = 5);
   if (ctx->variant == 0 && launch_step_lean(ctx, mode, s)) return void(ctx->last_kernel = 2);
   StepArgs t = s;
   t.push = nullptr;

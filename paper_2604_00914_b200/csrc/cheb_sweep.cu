@@ -151,6 +151,22 @@ void build_stencil_plan(adp_csr* a, int64_t goff, StencilPlan& p) {
     }
     if (e != e1) return void(p.why = "row " + std::to_string(r) + ": extra entries");
   }
+  // shared class products: 27-point weights that depend only on the distance class m (bitwise equal
+  // within a class); 7-point neighbour weights all exactly -1
+  auto same = [](double u, double v) { return std::memcmp(&u, &v, sizeof u) == 0; };
+  p.classes = true;
+  bool seen[4] = {};
+  for (const Off& o : set) {
+    const int idx = (o.dz + 1) * 9 + (o.dy + 1) * 3 + (o.dx + 1);
+    const int m = std::abs(o.dx) + std::abs(o.dy) + std::abs(o.dz);
+    if (m == 0) continue;
+    if (!have[idx]) p.classes = false;  // an offset no row holds: keep the general path
+    if (p.kind == 7 && !same(p.w[idx], -1.0)) p.classes = false;
+    if (p.kind == 27) {
+      if (!seen[m]) p.cls[m] = p.w[idx], seen[m] = true;
+      if (!same(p.cls[m], p.w[idx])) p.classes = false;
+    }
+  }
   ADP_CUDA(cudaMalloc(&p.d_diag, diag.size() * sizeof(double)));
   ADP_CUDA(cudaMemcpy(p.d_diag, diag.data(), diag.size() * sizeof(double), cudaMemcpyHostToDevice));
   plan_uploads_done();
@@ -214,7 +230,15 @@ __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* tm, int32_t 
 __device__ __forceinline__ void st_hint(void* ptr, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(ptr), "d"(v), "l"(pol) : "memory");
 }
-__device__ __forceinline__ double mac(double acc, double v, double w) { return __dadd_rn(acc, __dmul_rn(v, w)); }
+// Product arithmetic of the sweep kernel, all the reference's unfused SSE2 rounding: kExact: every
+// product rounded then added; kShared: the same, with each distance-class product formed once per
+// loaded W value; kUnitNeg: the 7-point star with all neighbour weights -1 (subtractions). (A DFMA
+// variant measured the same sustained time once the product count was shared: not kept.)
+constexpr int kExact = 0, kShared = 1, kUnitNeg = 2;
+template <int ARITH>
+__device__ __forceinline__ double mac(double acc, double v, double w) {
+  return __dadd_rn(acc, __dmul_rn(v, w));
+}
 
 // ---- the kernel -----------------------------------------------------------------------------
 constexpr int kTX = 8;   // grid points per thread along x
@@ -246,13 +270,14 @@ struct SwArgs {
   int32_t tiles_x, tiles_y, n_items;
   double s0, s1, s2;
   double w[27];  // constant values by offset; read as constant-bank operands of the DMULs
+  double c[4];   // kShared: the value of distance class m = |dx| + |dy| + |dz| (m = 1..3)
   // peer-memory halo (multi-GPU row partition): output rows r in [lo, hi) are also stored to
   // dst + (r + shift) * ld_b, a neighbour's halo rows mapped over NVLink (see cheb_lean.cu)
   PushTarget push[kMaxPush];
   int32_t n_push;
 };
 
-template <int NW, int KIND>
+template <int NW, int KIND, int ARITH, bool PUSH>
 __global__ void __launch_bounds__((NW + 1) * 32, 1)
     cheb_sweep_kernel(const __grid_constant__ SwArgs p, const __grid_constant__ CUtensorMap tm_w,
                       const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_v,
@@ -336,7 +361,34 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
         mbar_wait(full_w + sw, pw);
         const double* ws = reinterpret_cast<const double*>(smem + sw * G::kWS);
         const double* ds = reinterpret_cast<const double*>(smem + sw * G::kWS + G::kW) + yl * kTX;
-        if constexpr (KIND == 27) {
+        if constexpr (KIND == 27 && ARITH == kShared) {
+          // weights depend only on m = |dx| + |dy| + |dz| (c1 faces, c2 edges, c3 corners): each loaded W
+          // value's products c_m * w are rounded ONCE and added by every output that holds it at class m
+          // -- the same rounded product the reference forms per entry, so the sums are bitwise its own
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy) {
+            double w[kTX + 2], p1[kTX + 2], p2[kTX + 2], p3[kTX + 2];
+            const double* row = ws + (yl + dy) * G::WX * kPW + lane;
+#pragma unroll
+            for (int i = 0; i < kTX + 2; ++i) {
+              w[i] = row[i * kPW];
+              p1[i] = __dmul_rn(p.c[1], w[i]);
+              p2[i] = __dmul_rn(p.c[2], w[i]);
+              if (dy != 1) p3[i] = __dmul_rn(p.c[3], w[i]);
+            }
+#pragma unroll
+            for (int x = 0; x < kTX; ++x) {
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx) {
+                const int i = x + dx, m = (dx != 1) + (dy != 1);  // in-plane distance class
+                const double pz = m == 0 ? p1[i] : (m == 1 ? p2[i] : p3[i]);  // class m + 1 (dz = -1, +1)
+                hi[x] = __dadd_rn(hi[x], pz);
+                mid[x] = __dadd_rn(mid[x], m == 0 ? __dmul_rn(ds[x], w[i]) : (m == 1 ? p1[i] : p2[i]));
+                lo[x] = __dadd_rn(lo[x], pz);
+              }
+            }
+          }
+        } else if constexpr (KIND == 27) {
 #pragma unroll
           for (int dy = 0; dy < 3; ++dy) {
             double w[kTX + 2];
@@ -348,9 +400,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx) {
                 const double wv = w[x + dx];
-                hi[x] = mac(hi[x], p.w[dy * 3 + dx], wv);  // dz = -1 entries of plane wz+1
-                mid[x] = mac(mid[x], (dy == 1 && dx == 1) ? ds[x] : p.w[9 + dy * 3 + dx], wv);
-                lo[x] = mac(lo[x], p.w[18 + dy * 3 + dx], wv);  // dz = +1 entries of plane wz-1
+                hi[x] = mac<ARITH>(hi[x], p.w[dy * 3 + dx], wv);  // dz = -1 entries of plane wz+1
+                mid[x] = mac<ARITH>(mid[x], (dy == 1 && dx == 1) ? ds[x] : p.w[9 + dy * 3 + dx], wv);
+                lo[x] = mac<ARITH>(lo[x], p.w[18 + dy * 3 + dx], wv);  // dz = +1 entries of plane wz-1
               }
             }
           }
@@ -361,15 +413,29 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
           double w[kTX + 2];
 #pragma unroll
           for (int i = 0; i < kTX + 2; ++i) w[i] = ce[i * kPW];
+          if constexpr (ARITH == kUnitNeg) {
+            // every neighbour weight is exactly -1: acc + (-1 * w) == acc - w bitwise (IEEE x - y = x + (-y))
 #pragma unroll
-          for (int x = 0; x < kTX; ++x) {
-            hi[x] = mac(hi[x], p.w[4], w[x + 1]);
-            mid[x] = mac(mid[x], p.w[10], up[(x + 1) * kPW]);
-            mid[x] = mac(mid[x], p.w[12], w[x]);
-            mid[x] = mac(mid[x], ds[x], w[x + 1]);
-            mid[x] = mac(mid[x], p.w[14], w[x + 2]);
-            mid[x] = mac(mid[x], p.w[16], dn[(x + 1) * kPW]);
-            lo[x] = mac(lo[x], p.w[22], w[x + 1]);
+            for (int x = 0; x < kTX; ++x) {
+              hi[x] = __dsub_rn(hi[x], w[x + 1]);
+              mid[x] = __dsub_rn(mid[x], up[(x + 1) * kPW]);
+              mid[x] = __dsub_rn(mid[x], w[x]);
+              mid[x] = __dadd_rn(mid[x], __dmul_rn(ds[x], w[x + 1]));
+              mid[x] = __dsub_rn(mid[x], w[x + 2]);
+              mid[x] = __dsub_rn(mid[x], dn[(x + 1) * kPW]);
+              lo[x] = __dsub_rn(lo[x], w[x + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int x = 0; x < kTX; ++x) {
+              hi[x] = mac<ARITH>(hi[x], p.w[4], w[x + 1]);
+              mid[x] = mac<ARITH>(mid[x], p.w[10], up[(x + 1) * kPW]);
+              mid[x] = mac<ARITH>(mid[x], p.w[12], w[x]);
+              mid[x] = mac<ARITH>(mid[x], ds[x], w[x + 1]);
+              mid[x] = mac<ARITH>(mid[x], p.w[14], w[x + 2]);
+              mid[x] = mac<ARITH>(mid[x], p.w[16], dn[(x + 1) * kPW]);
+              lo[x] = mac<ARITH>(lo[x], p.w[22], w[x + 1]);
+            }
           }
         }
       }
@@ -389,11 +455,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
                   __dadd_rn(__dsub_rn(__dadd_rn(__dmul_rn(p.s0, lo[x]), __dmul_rn(p.s1, own[x * kPW])), vs[x * kPW]),
                             __dmul_rn(p.s2, ys[x * kPW]));
               st_hint(ob + static_cast<uint64_t>(x) * p.ldo_b, res, pol);
-              for (int tgt = 0; tgt < p.n_push; ++tgt) {  // uniform: one plane's rows are all in or all out
-                const int64_t r = rrow + x;
-                if (r >= p.push[tgt].lo && r < p.push[tgt].hi)
-                  *reinterpret_cast<double*>(p.push[tgt].dst + static_cast<uint64_t>(r + p.push[tgt].shift) *
-                                                                   p.push[tgt].ld_b + static_cast<uint64_t>(c) * 8) = res;
+              if constexpr (PUSH) {  // rows a neighbour needs, also into its halo (peer memory over NVLink)
+                for (int tgt = 0; tgt < p.n_push; ++tgt) {
+                  const int64_t r = rrow + x;
+                  if (r >= p.push[tgt].lo && r < p.push[tgt].hi)
+                    *reinterpret_cast<double*>(p.push[tgt].dst + static_cast<uint64_t>(r + p.push[tgt].shift) *
+                                                                     p.push[tgt].ld_b + static_cast<uint64_t>(c) * 8) = res;
+                }
               }
             }
           }
@@ -428,7 +496,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
 #pragma unroll
     for (int x = 0; x < kTX; ++x) A0[x] = A1[x] = A2[x] = 0.0;
   }
-  if (p.n_push) __threadfence_system();  // the peer stores are performed before the signal kernel that follows
+  if (PUSH) __threadfence_system();  // the peer stores are performed before the signal kernel that follows
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -466,7 +534,7 @@ CUtensorMap block_map(const void* base, const StencilPlan& sp, int64_t planes, i
   return make_map(4, base, dims, strides, box);
 }
 
-template <int NW, int KIND>
+template <int NW, int KIND, int ARITH, bool PUSH = false>
 void launch_sweep(adp_ctx* ctx, const StepArgs& s, const StencilPlan& sp) {
   using G = Geo<NW>;
   const int64_t plane = sp.nx * sp.ny;
@@ -490,6 +558,7 @@ void launch_sweep(adp_ctx* ctx, const StepArgs& s, const StencilPlan& sp) {
   k.s1 = s.s1;
   k.s2 = s.s2;
   for (int i = 0; i < 27; ++i) k.w[i] = sp.w[i];
+  for (int i = 0; i < 4; ++i) k.c[i] = sp.cls[i];
   k.n_push = s.n_push;
   for (int t = 0; t < s.n_push; ++t) k.push[t] = s.push[t];
   const CUtensorMap tm_w = block_map(s.gsrc, sp, sp.nzw, s.q, s.ld * 8, kTX + 2, NW + 2);
@@ -500,7 +569,7 @@ void launch_sweep(adp_ctx* ctx, const StepArgs& s, const StencilPlan& sp) {
   const cuuint64_t dstr[2] = {static_cast<cuuint64_t>(sp.nxp * 8), static_cast<cuuint64_t>(sp.nxp * sp.ny * 8)};
   const cuuint32_t dbox[3] = {kTX, NW, 1};
   const CUtensorMap tm_d = make_map(3, sp.d_diag, ddims, dstr, dbox);
-  auto kern = cheb_sweep_kernel<NW, KIND>;
+  auto kern = cheb_sweep_kernel<NW, KIND, ARITH, PUSH>;
   static_assert(G::kSmem <= 227 * 1024, "sweep kernel shared memory");
   ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(G::kSmem)));
   const int grid = static_cast<int>(std::min<int64_t>(k.n_items, ctx->sm_count));
@@ -524,14 +593,28 @@ bool launch_step_sweep(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
   if (mode != StepMode::Step || a->dtype != ADP_F64) return false;
   if (ctx->variant == 0 && !ctx->auto_sweep) return false;
+  if (ctx->variant != 0 && ctx->variant != 5) return false;
   if (a->nnz > 27 * a->n_rows || a->nnz < 2 * a->n_rows || s.row_end <= s.row_begin) return false;
   if (s.q < 1 || s.q >= (int64_t{1} << 31) || s.ld % 2 || s.ld_y % 2) return false;
   const StencilPlan* sp = get_stencil_plan(const_cast<adp_csr*>(a), s.goff);
   if (!sp->valid) return false;
   const int64_t plane = sp->nx * sp->ny;
   if (s.row_begin % plane || s.row_end % plane) return false;  // whole grid planes only
-  if (sp->kind == 27) launch_sweep<8, 27>(ctx, s, *sp);
-  else launch_sweep<8, 7>(ctx, s, *sp);
+  if (s.n_push) {  // boundary planes of a row partition, stored into the neighbours' halos too
+    if (sp->kind == 27) {
+      if (sp->classes) launch_sweep<8, 27, kShared, true>(ctx, s, *sp);
+      else launch_sweep<8, 27, kExact, true>(ctx, s, *sp);
+    } else {
+      if (sp->classes) launch_sweep<8, 7, kUnitNeg, true>(ctx, s, *sp);
+      else launch_sweep<8, 7, kExact, true>(ctx, s, *sp);
+    }
+  } else if (sp->kind == 27) {
+    if (sp->classes) launch_sweep<8, 27, kShared>(ctx, s, *sp);
+    else launch_sweep<8, 27, kExact>(ctx, s, *sp);
+  } else {
+    if (sp->classes) launch_sweep<8, 7, kUnitNeg>(ctx, s, *sp);
+    else launch_sweep<8, 7, kExact>(ctx, s, *sp);
+  }
   return true;
 }
 

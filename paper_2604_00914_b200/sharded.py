@@ -180,9 +180,9 @@ class TorchOps(NumpyOps):
         low, info = t.linalg.cholesky_ex(g)
         if int(info.item()) != 0:
             return None
-        r = low.conj().T.contiguous()
+        r = low.mH.resolve_conj().contiguous()
         d = t.real(t.diagonal(r))
-        if not bool(t.isfinite(t.view_as_real(r) if self.cplx else r).all()) or not bool((d > 0.0).all()):
+        if not bool(t.isfinite(r).all()) or not bool((d > 0.0).all()):
             return None
         return r
 

@@ -31,8 +31,13 @@ def ctx():
     c.close()
 
 
-def grid_operator(kind, nx, ny, nz, seed=0):
+def grid_operator(kind, nx, ny, nz, seed=0, general=False):
+    """A kind-point stencil with a Philox potential. The configs' weights (Mehrstellen 27-point: one value
+    per distance class -> the kernel's shared class products; 7-point: all -1 -> subtractions), or with
+    ``general`` one distinct value per offset (the kernel's per-offset product path)."""
     offs, ws = configs._twenty_seven_point() if kind == 27 else configs._seven_point()
+    if general:
+        ws = [-(0.3 + 0.05 * j) for j in range(len(offs))]
     u = adp.philox_uniform(seed, configs.STREAM_POTENTIAL, 0, nx * ny * nz)
     centre = ws[13] if kind == 27 else 6.0
     return configs.stencil_3d(nx, offs, ws, centre - 2.0 + 4.0 * u, ny=ny, nz=nz)
@@ -70,10 +75,11 @@ def test_stencil_detection(ctx, orc):
     assert adp.DeviceCsr(configs.peierls_lattice(20), ctx).stencil()[0] == 0
 
 
-@pytest.mark.parametrize("kind,dims", [(27, (9, 5, 7)), (27, (16, 8, 4)), (27, (10, 11, 3)), (7, (13, 17, 6)),
-                                       (7, (8, 8, 8)), (7, (21, 3, 5))])
-def test_sweep_bitwise_shapes(ctx, orc, kind, dims):
-    a = grid_operator(kind, *dims, seed=sum(dims))
+@pytest.mark.parametrize("kind,dims,general", [(27, (9, 5, 7), False), (27, (16, 8, 4), False), (27, (10, 11, 3), False),
+                                               (7, (13, 17, 6), False), (7, (8, 8, 8), False), (7, (21, 3, 5), False),
+                                               (27, (9, 5, 7), True), (7, (13, 17, 6), True)])
+def test_sweep_bitwise_shapes(ctx, orc, kind, dims, general):
+    a = grid_operator(kind, *dims, seed=sum(dims), general=general)
     da = adp.DeviceCsr(a, ctx)
     assert da.stencil() == (kind, dims)
     bounds = (-12.0, 16.0) if kind == 27 else (-3.0, 15.0)

@@ -56,7 +56,7 @@ def test_tma_and_async_copies_present(sass):
     # the plane sweep: W halo tiles, the diagonal and the V / Y tiles as 4-D / 3-D tensor-map tiles,
     # consumed from shared memory (LDS), completion on mbarriers
     sweep = [f for f in funcs if "cheb_sweep_kernel" in f]
-    assert len(sweep) == 2
+    assert len(sweep) >= 4
     for f in sweep:
         assert any("UTMALDG" in ln for ln in funcs[f]) and any("LDS" in ln for ln in funcs[f])
         assert any("SYNCS" in ln for ln in funcs[f])

@@ -20,11 +20,11 @@ from paper_2604_00914_b200 import configs  # noqa: E402
 
 def sampler(samples, stop):
     while not stop.is_set():
-        out = subprocess.run(["nvidia-smi", "--query-gpu=power.draw,clocks.sm,temperature.gpu",
+        out = subprocess.run(["nvidia-smi", "--query-gpu=power.draw,clocks.sm,temperature.gpu,clocks.mem",
                               "--format=csv,noheader,nounits", "-i", "0"], capture_output=True, text=True).stdout
         try:
-            pw, sm, tc = (float(v) for v in out.strip().split(","))
-            samples.append((pw, sm, tc))
+            pw, sm, tc, mem = (float(v) for v in out.strip().split(","))
+            samples.append((pw, sm, tc, mem))
         except ValueError:
             pass
         time.sleep(0.1)
@@ -33,7 +33,7 @@ def sampler(samples, stop):
 def summarize(samples):
     s = samples[len(samples) // 4:]  # skip the ramp
     med = lambda i: sorted(v[i] for v in s)[len(s) // 2] if s else float("nan")  # noqa: E731
-    return f"power {med(0):.0f} W, sm {med(1):.0f} MHz, temp {med(2):.0f} C ({len(samples)} samples)"
+    return f"power {med(0):.0f} W, sm {med(1):.0f} MHz, mem {med(3):.0f} MHz, temp {med(2):.0f} C ({len(samples)} samples)"
 
 
 def copy_probe(seconds):
