@@ -48,7 +48,8 @@ sys.path.insert(0, ROOT)
 METRIC = "Chebyshev-filter SpMM effective HBM GB/s (% of peak); end-to-end solve time"  # BASELINE.json metric
 KERNELS = {1: "cheb_step_kernel (csrc/cheb_step.cu)", 2: "cheb_lean_kernel (csrc/cheb_lean.cu)",
            3: "cheb_line_kernel (csrc/cheb_line.cu)", 4: "cheb_cube_kernel (csrc/cheb_cube.cu)",
-           5: "cheb_sweep_kernel (csrc/cheb_sweep.cu: plane-sweep stencil, 4-D TMA halo tiles)"}
+           5: "cheb_sweep_kernel (csrc/cheb_sweep.cu: plane-sweep stencil, 4-D TMA halo tiles)",
+           6: "cheb_band_kernel (csrc/cheb_band.cu: band-block sweep, W row panels shared by 8 rows)"}
 
 
 def parse_args():

@@ -72,7 +72,7 @@ adp_status adp_ctx_synchronize(adp_ctx* ctx);
 /* Number of kernels this library has launched on ctx (instrumentation for bench.py). */
 int64_t adp_ctx_launch_count(const adp_ctx* ctx);
 /* Kernel family of the last fused-step launch on ctx (1 row, 2 lean, 3 line, 4 cube,
- * 5 plane sweep; 0 none yet) -- instrumentation for tests and bench.py. */
+ * 5 plane sweep, 6 band; 0 none yet) -- instrumentation for tests and bench.py. */
 int32_t adp_ctx_last_step_kernel(const adp_ctx* ctx);
 /* Kernel tuning knobs (0 = automatic): columns per warp task (panel width). */
 adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
@@ -82,8 +82,10 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
  * 3 line kernel (register reuse across shifted-pattern row blocks), 4 cube kernel
  * (runs shared by 2-D/3-D blocks of grid lines), 5 plane-sweep stencil kernel
  * (constant-coefficient 3-D stencils: halo tiles of W streamed plane by plane
- * through shared memory). A family that does not apply to an operator falls
- * back to the next one. Other values fail with ADP_ERR_CONFIG. */
+ * through shared memory), 6 band-block kernel (banded operators with sparse
+ * off-band entries: W row panels shared by 8 consecutive rows), 7 the same with
+ * 4-row blocks. A family that does not apply to an operator falls back to the
+ * next one. Other values fail with ADP_ERR_CONFIG. */
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant);
 
 /* -------------------------------------------------------------- operator -- */

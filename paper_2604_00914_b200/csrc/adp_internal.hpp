@@ -61,14 +61,16 @@ struct adp_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // where work is queued (own or borrowed)
+  cudaStream_t copy_stream = nullptr;  // host-API pipelining: chunk copies beside the filter (lazy)
   int sm_count = 148;
   int64_t launches = 0;
   int panel_cols = 0;  // 0 = automatic
-  int variant = 0;     // kernel family (adp_ctx_set_tuning): 0 automatic, 1 row, 2 lean, 3 line, 4 cube, 5 sweep
+  int variant = 0;     // kernel family (adp_ctx_set_tuning): 0 automatic, 1 row, 2 lean, 3 line, 4 cube, 5 sweep, 6 band
   bool pdl = true;        // programmatic dependent launch between degree steps (ADP_NO_PDL=1: off)
   bool auto_line = true;  // automatic line-kernel choice (ADP_NO_LINE=1: off, for A/B timing)
   bool auto_cube = true;  // automatic cube-kernel choice for its full panels (ADP_NO_CUBE=1: off)
   bool auto_sweep = true; // automatic plane-sweep stencil kernel (ADP_NO_SWEEP=1: off)
+  bool auto_band = true;  // automatic band-block kernel (ADP_NO_BAND=1: off)
   int last_kernel = 0;    // family of the last step launch (adp_ctx_last_step_kernel)
   adp::DevBuf ws[6];   // scratch: staging, Y, W, V, misc
   void* cublas = nullptr;
@@ -133,6 +135,14 @@ struct StencilPlan {
   std::string why;            // why the operator is not such a stencil (diagnostics)
   ~StencilPlan();
 };
+// A banded operator with sparse off-band entries (cheb_band.cu): every row r holds all columns
+// max(0, r - h) .. min(n - 1, r + h), preceded by nlow[r] and followed by the rest of its entries.
+struct BandPlan {
+  bool valid = false;
+  int64_t h = 0;
+  int32_t* d_nlow = nullptr;  // [n] entries before the band
+  ~BandPlan();
+};
 }  // namespace adp
 
 struct adp_csr {
@@ -152,6 +162,7 @@ struct adp_csr {
   std::vector<std::unique_ptr<adp::LinePlan>> line_plans;
   std::vector<std::unique_ptr<adp::CubePlan>> cube_plans;
   std::unique_ptr<adp::StencilPlan> stencil;  // built on first use (cheb_sweep.cu)
+  std::unique_ptr<adp::BandPlan> band;        // built on first use (cheb_band.cu)
 };
 
 namespace adp {
@@ -241,6 +252,9 @@ const CubePlan* get_cube_plan(adp_csr* a, int rows_per_line, int ly, int lz, int
 // operators (StencilPlan). Returns false if not applicable.
 bool launch_step_sweep(adp_ctx* ctx, StepMode mode, const StepArgs& args);
 const StencilPlan* get_stencil_plan(adp_csr* a, int64_t goff = 0);
+// The band-block kernel (cheb_band.cu): Step launches on banded operators (config 5).
+bool launch_step_band(adp_ctx* ctx, StepMode mode, const StepArgs& args);
+const BandPlan* get_band_plan(adp_csr* a);
 // Host copies of a device-created operator's arrays, downloaded on first use by the
 // host-side preprocessing (line plans, tilings, segments, the dense fallback).
 void ensure_host_copy(adp_csr* a);

@@ -161,6 +161,102 @@ void download_block(adp_ctx* ctx, const void* dev, int64_t ldd, int64_t n, int64
     ADP_CUDA(cudaMemcpy2DAsync(host, ldh * eb, staging, n * eb, n * eb, q, cudaMemcpyDeviceToHost, ctx->stream));
 }
 
+// The host-API filter on a large block, pipelined over column chunks (columns are independent:
+// every chunk's result is bitwise the whole call's): chunk k + 1's H2D copy and layout transpose
+// run on a copy stream while chunk k filters on the context's stream, and chunk k's transpose back
+// and D2H copy overlap chunk k + 1's filter. Device memory: 6 chunk blocks instead of 4 full blocks.
+void filter_apply_pipelined(adp_ctx* ctx, const adp_csr* a, const double* coeffs, double l1, double l2, int deg,
+                            const void* x, int64_t ldx, int64_t q, adp_layout layout, void* y, int64_t ldy,
+                            size_t eb) {
+  const int64_t n = a->n_rows;
+  const int64_t cw = std::min<int64_t>(q, ((q + 3) / 4 + 63) / 64 * 64);  // ~4 chunks, whole 64-column panels
+  const int64_t nchunks = (q + cw - 1) / cw;
+  const int64_t ld = ws_ld(a, cw);
+  const size_t blk = static_cast<size_t>(n) * ld * eb, stg = static_cast<size_t>(n) * cw * eb;
+  char* yb[2] = {static_cast<char*>(ctx->ws[1].get(blk)), static_cast<char*>(ctx->ws[4].get(blk))};
+  void* wbuf = ctx->ws[2].get(blk);
+  void* vbuf = ctx->ws[3].get(blk);
+  char* st_in[2];
+  char* st_out[2];
+  char* stage = static_cast<char*>(ctx->ws[0].get(4 * stg));
+  for (int i = 0; i < 2; ++i) {
+    st_in[i] = stage + i * stg;
+    st_out[i] = stage + (2 + i) * stg;
+  }
+  if (!ctx->copy_stream) ADP_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = ctx->copy_stream, ms = ctx->stream;
+  std::vector<cudaEvent_t> ev;
+  auto event = [&]() {
+    cudaEvent_t e;
+    ADP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+    return e;
+  };
+  struct Guard {
+    std::vector<cudaEvent_t>& ev;
+    ~Guard() {
+      for (auto e : ev) cudaEventDestroy(e);
+    }
+  } guard{ev};
+  cudaEvent_t start = event();
+  ADP_CUDA(cudaEventRecord(start, ms));  // the copy stream starts after the caller's prior work
+  ADP_CUDA(cudaStreamWaitEvent(cs, start, 0));
+  const char* xh = static_cast<const char*>(x);
+  char* yh = static_cast<char*>(y);
+  std::vector<cudaEvent_t> up(nchunks), comp(nchunks), ready(nchunks), down(nchunks);
+  for (int64_t k = 0; k < nchunks; ++k) {
+    up[k] = event();
+    comp[k] = event();
+    ready[k] = event();
+    down[k] = event();
+  }
+  auto upload = [&](int64_t k) {  // host chunk k -> yb[k % 2] (copy stream)
+    const int64_t c0 = k * cw, qc = std::min(cw, q - c0);
+    if (k >= 2) ADP_CUDA(cudaStreamWaitEvent(cs, comp[k - 2], 0));  // yb[k % 2] free
+    struct OnCopyStream {  // the layout kernels of the upload run on the copy stream
+      adp_ctx* c;
+      cudaStream_t saved;
+      ~OnCopyStream() { c->stream = saved; }
+    } on{ctx, ms};
+    ctx->stream = cs;
+    if (ld != qc) ADP_CUDA(cudaMemsetAsync(yb[k % 2], 0, blk, cs));
+    if (layout == ADP_COL_MAJOR)
+      upload_block(ctx, xh + c0 * ldx * eb, n, qc, ldx, layout, yb[k % 2], ld, st_in[k % 2], eb);
+    else
+      upload_block(ctx, xh + c0 * eb, n, qc, ldx, layout, yb[k % 2], ld, st_in[k % 2], eb);
+    ADP_CUDA(cudaEventRecord(up[k], cs));
+  };
+  upload(0);
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int64_t c0 = k * cw, qc = std::min(cw, q - c0);
+    if (k + 1 < nchunks) upload(k + 1);
+    ADP_CUDA(cudaStreamWaitEvent(ms, up[k], 0));
+    void* obuf = (deg % 2 == 0) ? wbuf : vbuf;
+    clenshaw_device(ctx, a, coeffs, l1, l2, deg, yb[k % 2], ld, obuf, ld, wbuf, vbuf, ld, qc);
+    ADP_CUDA(cudaEventRecord(comp[k], ms));
+    // transpose out on the compute stream (before the next chunk reuses W / V), then D2H on the copy stream
+    if (k >= 2) ADP_CUDA(cudaStreamWaitEvent(ms, down[k - 2], 0));  // st_out[k % 2] free
+    char* host_k = layout == ADP_COL_MAJOR ? yh + c0 * ldy * eb : yh + c0 * eb;
+    if (layout == ADP_COL_MAJOR) {
+      launch_rowmajor_to_colmajor(ctx, obuf, n, qc, ld, st_out[k % 2], n, static_cast<int>(eb));
+      ADP_CUDA(cudaEventRecord(ready[k], ms));
+      ADP_CUDA(cudaStreamWaitEvent(cs, ready[k], 0));
+      if (ldy == n)
+        ADP_CUDA(cudaMemcpyAsync(host_k, st_out[k % 2], n * qc * eb, cudaMemcpyDeviceToHost, cs));
+      else
+        ADP_CUDA(cudaMemcpy2DAsync(host_k, ldy * eb, st_out[k % 2], n * eb, n * eb, qc, cudaMemcpyDeviceToHost, cs));
+    } else {
+      ADP_CUDA(cudaMemcpy2DAsync(st_out[k % 2], qc * eb, obuf, ld * eb, qc * eb, n, cudaMemcpyDeviceToDevice, ms));
+      ADP_CUDA(cudaEventRecord(ready[k], ms));
+      ADP_CUDA(cudaStreamWaitEvent(cs, ready[k], 0));
+      ADP_CUDA(cudaMemcpy2DAsync(host_k, ldy * eb, st_out[k % 2], qc * eb, qc * eb, n, cudaMemcpyDeviceToHost, cs));
+    }
+    ADP_CUDA(cudaEventRecord(down[k], cs));
+  }
+  ADP_CUDA(cudaStreamSynchronize(cs));
+  ADP_CUDA(cudaStreamSynchronize(ms));
+}
+
 }  // namespace
 
 void set_last_error(const std::string& m) { g_last_error = m; }
@@ -199,6 +295,8 @@ adp_status adp_ctx_create(int32_t device, adp_ctx** out) {
     ctx->auto_cube = !(no_cube && no_cube[0] == '1');
     const char* no_sweep = std::getenv("ADP_NO_SWEEP");
     ctx->auto_sweep = !(no_sweep && no_sweep[0] == '1');
+    const char* no_band = std::getenv("ADP_NO_BAND");
+    ctx->auto_band = !(no_band && no_band[0] == '1');
     *out = ctx;
   });
 }
@@ -213,6 +311,7 @@ adp_status adp_ctx_destroy(adp_ctx* ctx) {
     adp_release_dense_handles(ctx);
     for (auto& b : ctx->ws) b.release();
     if (ctx->halo_failed) cudaFree(ctx->halo_failed);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
   });
@@ -259,7 +358,7 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
   return guarded([&] {
     // 0 automatic; 1-5 force one kernel family (adp.h)
-    if (variant < 0 || variant > 5) fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
+    if (variant < 0 || variant > 7) fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
   });
 }
@@ -455,6 +554,11 @@ adp_status adp_filter_apply(adp_ctx* ctx, const adp_csr* a, const double* coeffs
     const int deg = effective_degree(coeffs, degree);
     if (spmv_count) *spmv_count += static_cast<int64_t>(deg) * q;
     const size_t eb = elem_bytes(a);
+    if (deg >= 2 && q >= 256 && static_cast<size_t>(n) * q * eb >= (size_t{1} << 30)) {
+      // large blocks: column chunks with their host copies overlapped with the previous chunk's filter
+      filter_apply_pipelined(ctx, a, coeffs, l1, l2, deg, x, ldx, q, layout, y, ldy, eb);
+      return;
+    }
     const int64_t ld = ws_ld(a, q);
     const size_t blk = static_cast<size_t>(n) * ld * eb;
     void* staging = ctx->ws[0].get(static_cast<size_t>(n) * q * eb);

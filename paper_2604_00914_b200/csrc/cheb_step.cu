@@ -388,11 +388,13 @@ void launch_step_impl(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   if (s.row_end <= s.row_begin || s.q == 0) return;
   // Dispatch (variant 0 = automatic; adp_ctx_set_tuning forces one family):
   // the plane-sweep stencil kernel (cheb_sweep.cu) for Step launches on operators that are
-  // a constant-coefficient 3-D stencil plus a diagonal; the cube / line kernels for other
+  // a constant-coefficient 3-D stencil plus a diagonal; the band-block kernel (cheb_band.cu) for
+  // banded operators with sparse off-band entries (config 5); the cube / line kernels for other
   // long-row stencils (cheb_cube.cu, cheb_line.cu); the lean kernel (cheb_lean.cu) for
   // >= 4 vectors; this file's narrow-group row kernel for 1-3 vectors and variant 1.
   const int v = ctx->variant;
   if ((v == 0 || v == 5) && launch_step_sweep(ctx, mode, s)) return void(ctx->last_kernel = 5);
+  if ((v == 0 || v == 6 || v == 7) && launch_step_band(ctx, mode, s)) return void(ctx->last_kernel = 6);
   if (v == 4 && launch_step_cube(ctx, mode, s)) return void(ctx->last_kernel = 4);
   if ((v == 0 || v == 3) && launch_step_line(ctx, mode, s)) return void(ctx->last_kernel = 3);
   if (v != 1 && launch_step_lean(ctx, mode, s)) return void(ctx->last_kernel = 2);

@@ -38,13 +38,10 @@ import time
 
 import numpy as np
 
+from ._native import ConfigError
 from .filter import SpectrumBounds, adaptive_degree, build_filter, initial_degree
 from .solver import IterationRecord, SolveResult, SolverConfig, StageTimings
-from .sparse import philox_gaussian, fill_rademacher
-
-
-class ConfigError(ValueError):
-    pass
+from .sparse import fill_rademacher, philox_gaussian
 
 
 # ---------------------------------------------------------------------------- comms ---

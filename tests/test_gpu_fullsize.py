@@ -112,3 +112,29 @@ def test_bench_degree_columns_bitwise_vs_oracle(ctx, orc, name, cols):
     del x, y
     da.close()
     torch.cuda.empty_cache()
+
+
+def test_host_api_pipelined_chunks_equal_device_api(ctx):
+    # blocks >= 1 GB go through the host API in column chunks whose copies overlap the previous chunk's
+    # filter (capi.cu filter_apply_pipelined); columns are independent, so every bit must equal the
+    # device API's single call -- column-major (Eigen) and row-major host layouts, a ragged last chunk
+    cfg = configs.CONFIGS["c2"]
+    a = cfg.operator()
+    da = adp.DeviceCsr(a, ctx)
+    f = adp.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, 40, 0.5)
+    for q in (256, 301):
+        x = device_block(ctx, a.n_rows, q + (q % 2), seed=q)[:, :q]
+        yd = adp.clenshaw_apply_device(f, da, x, 7).cpu().numpy()
+        xh = x.cpu().numpy()
+        yh = adp.clenshaw_apply(f, da, np.asfortranarray(xh), 7)
+        assert np.array_equal(yd, yh), q
+        lib = _native.lib()
+        xr = np.ascontiguousarray(xh)
+        yr = np.empty_like(xr)
+        coeffs = f.coeff_array()
+        cnt = C.c_int64(0)
+        _native.check(lib.adp_filter_apply(ctx.h, da.h, coeffs.ctypes.data_as(C.c_void_p), f.k_max, f.l1, f.l2, 7,
+                                           xr.ctypes.data_as(C.c_void_p), a.n_rows, q, q, 1,
+                                           yr.ctypes.data_as(C.c_void_p), q, C.byref(cnt)))
+        assert np.array_equal(yd, yr), q
+        assert cnt.value == 7 * q

@@ -282,12 +282,12 @@ def test_config2_full_size_bitwise_low_degree(ctx, orc):
 
 # ------------------------------------------------- every kernel variant ---
 # Every kernel family (adp_ctx_set_tuning: 1 row, 2 lean, 3 line, 4 cube,
-# 5 plane sweep) must be bitwise equal to the oracle: they only reorganise
+# 5 plane sweep, 6 / 7 band blocks) must be bitwise equal to the oracle: they only reorganise
 # loads, never the per-element arithmetic. Stencil operators exercise the
 # shifted-pattern blocks (and their irregular faces) and the plane sweep
 # (grids not multiples of its 8 x 8 tiles), a random matrix the row-by-row
 # fallbacks.
-VARIANTS = [0, 1, 2, 3, 4, 5]
+VARIANTS = [0, 1, 2, 3, 4, 5, 6, 7]
 
 
 @pytest.mark.parametrize("kind", ["lap7", "lap27", "random", "hermitian", "band"])

@@ -25,7 +25,7 @@ import paper_2604_00914_b200 as adp  # noqa: E402
 from paper_2604_00914_b200 import configs  # noqa: E402
 import bench  # noqa: E402
 
-FP64_DFMA_TFLOPS = 37.0  # B200 nominal vector FP64 (FMA = 2 flops); DMUL / DADD issue at the same rate, 1 flop each
+FP64_DFMA_TFLOPS = bench.fp64_peak()[0]  # measured DFMA peak (profiles/fp64_peak.json), FMA = 2 flops
 
 
 def main():
@@ -34,12 +34,15 @@ def main():
     p.add_argument("--q", type=int, default=384)
     p.add_argument("--reps", type=int, default=2)
     p.add_argument("--out", default="gpurun_out/c5_full.json")
+    p.add_argument("--variant", type=int, default=0, help="kernel family (0 automatic: band-block kernel)")
+    p.add_argument("--n", type=int, default=4_000_000, help="rows (config 5: 4e6)")
     args = p.parse_args()
     cfg = configs.CONFIGS["c5"]
     ctx = adp.Context(0)
     ctx.set_stream(torch.cuda.current_stream())
+    ctx.set_tuning(args.variant)
     t0 = time.time()
-    rp, ci, v = cfg.device_build()
+    rp, ci, v = configs.random_banded_hermitian_device(args.n, 250, 20)
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     n, nnz = rp.numel() - 1, ci.numel()
@@ -99,7 +102,8 @@ def main():
         "hbm_peak": [peak_gbs, peak_src],
         "flops_per_step": flops,
         "fp64_tflops": round(tflops, 2),
-        "fp64_frac_of_unfused_issue_peak": round(tflops / (FP64_DFMA_TFLOPS / 2), 4),
+        "fp64_frac_of_dfma_peak": round(tflops / FP64_DFMA_TFLOPS, 4),
+        "step_kernel": ctx.last_step_kernel,
         "spectral_radius_power_iteration": round(rad, 3),
         "bounds_used": list(cfg.bounds),
         "window": list(cfg.window),
