@@ -79,6 +79,9 @@ struct adp_ctx {
 };
 
 namespace adp {
+// Leading dimension (elements) of a row-major device block of q columns: 16-byte aligned rows, and
+// whole 256-byte panels once the block is wider than one (ADP_WS_ALIGN overrides the fp64 column multiple).
+int64_t block_ld(int64_t q, bool cplx);
 // Shifted-pattern row blocks of an operator for the line kernel (cheb_line.cu).
 struct LinePlan {
   int R = 0, mm = 0;

@@ -14,6 +14,17 @@
 
 namespace adp {
 
+int64_t block_ld(int64_t q, bool cplx) {
+  static const int64_t align = [] {  // fp64 columns; 32 = one 256-byte panel
+    const char* e = std::getenv("ADP_WS_ALIGN");
+    const int64_t v = e ? std::atoll(e) : 32;
+    return v >= 2 && v % 2 == 0 ? v : 32;
+  }();
+  const int64_t m = cplx ? std::max<int64_t>(align / 2, 1) : align;  // elements per alignment unit
+  if (q > m) return (q + m - 1) / m * m;
+  return cplx ? q : ((q + 1) / 2) * 2;
+}
+
 namespace {
 thread_local std::string g_last_error;
 
@@ -38,7 +49,10 @@ size_t elem_bytes(const adp_csr* a) { return a->dtype == ADP_C128 ? 16 : 8; }
 
 // Row-major workspace leading dimension: even number of fp64 columns so every
 // row starts 16-byte aligned; complex rows are already 16-byte elements.
-int64_t ws_ld(const adp_csr* a, int64_t q) { return a->dtype == ADP_C128 ? q : ((q + 1) / 2) * 2; }
+// Blocks wider than one 256-byte panel round up to whole panels: every row (and every 32-column
+// panel of it) then starts on a 256-byte boundary -- with p = 926 columns (7408-byte rows) the sweep
+// kernel's TMA boxes straddle cache lines (ADP_WS_ALIGN=2 restores the minimal pitch for A/B timing).
+int64_t ws_ld(const adp_csr* a, int64_t q) { return block_ld(q, a->dtype == ADP_C128); }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -358,7 +372,7 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
   return guarded([&] {
     // 0 automatic; 1-5 force one kernel family (adp.h)
-    if (variant < 0 || variant > 7) fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
+    if (variant < 0 || variant > 9) fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
   });
 }

@@ -57,6 +57,7 @@ __global__ void band_plan_kernel(const RP* __restrict__ rp, const int32_t* __res
 struct RealB {
   using Val = double;
   static __device__ __forceinline__ Val load(const void* p, int64_t k) { return __ldg(static_cast<const double*>(p) + k); }
+  static __device__ __forceinline__ Val ldp(const Val* p) { return __ldg(p); }
   static __device__ __forceinline__ double2 mac(double2 acc, Val v, double2 w) {
     acc.x = __dadd_rn(acc.x, __dmul_rn(v, w.x));
     acc.y = __dadd_rn(acc.y, __dmul_rn(v, w.y));
@@ -66,6 +67,7 @@ struct RealB {
 struct CplxB {
   using Val = double2;
   static __device__ __forceinline__ Val load(const void* p, int64_t k) { return __ldg(static_cast<const double2*>(p) + k); }
+  static __device__ __forceinline__ Val ldp(const Val* p) { return __ldg(p); }
   static __device__ __forceinline__ double2 mac(double2 acc, Val v, double2 w) {  // as CplxL::mac (cheb_lean.cu)
     acc.x = __fma_rn(v.x, w.x, acc.x);
     acc.x = __fma_rn(-v.y, w.y, acc.x);
@@ -105,108 +107,242 @@ struct BArgs {
   double s0, s1, s2;
 };
 
-// One warp per (block of R consecutive rows, panel of 32 x CH 16-byte vectors); Step mode.
-template <class F, int R, int CH, class RP, int MINB>
-__global__ void __launch_bounds__(256, MINB) cheb_band_kernel(const BArgs p) {
-  const int lane = threadIdx.x & 31;
-  const int64_t task = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (task >= static_cast<int64_t>(p.n_blocks) * p.n_panels) return;  // warp-uniform
-  const int panel = static_cast<int>(task / p.n_blocks);
-  const int64_t r0 = (task - static_cast<int64_t>(panel) * p.n_blocks) * R;
-  const uint32_t voff = (static_cast<uint32_t>(panel) * 32 * CH + lane) * 16u;
-  bool ok[CH];
+constexpr int kCH = 2;  // 16-byte vectors per lane: a panel is 32 x kCH vectors (1 KB per row)
+constexpr int kPF = 2;  // band sweep: W row panels loaded this many columns ahead
+
+__device__ __forceinline__ double shfl_val(double v, int j) { return __shfl_sync(0xffffffffu, v, j); }
+__device__ __forceinline__ double2 shfl_val(double2 v, int j) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, j), __shfl_sync(0xffffffffu, v.y, j));
+}
+__device__ __forceinline__ double zero_val(double) { return 0.0; }
+__device__ __forceinline__ double2 zero_val(double2) { return make_double2(0.0, 0.0); }
+
+// Off-band entries [e0, e0 + cnt) of GR consecutive rows (warp-uniform e0 / cnt per row), entry by
+// entry in CSR order per row, the GR rows interleaved so GR x kCH gathers are in flight. Columns and
+// values are fetched 32 entries at a time (coalesced) and handed out by shuffles.
+template <class F, int GR>
+__device__ __forceinline__ void offband(const BArgs& p, const char* gb, const bool (&ok)[kCH], const int64_t (&e0)[GR],
+                                        const int32_t (&cnt)[GR], double2 (*acc)[kCH], int lane) {
+  using Val = typename F::Val;
+  int32_t maxcnt = 0;
 #pragma unroll
-  for (int c = 0; c < CH; ++c) ok[c] = panel * 32 * CH + c * 32 + lane < p.valid;
-  // row metadata (the operator is constant: read before the wait): band start entry, first band
-  // column and band length of each row
-  int64_t bs[R];
-  int32_t b0[R], blen[R];
+  for (int g = 0; g < GR; ++g) maxcnt = cnt[g] > maxcnt ? cnt[g] : maxcnt;
+  for (int32_t base = 0; base < maxcnt; base += 32) {
+    int32_t mc[GR];
+    Val mv[GR];
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int64_t r = r0 + i < p.n ? r0 + i : p.n - 1;
-    bs[i] = ld_rp<RP>(p.row_ptr, r) + __ldg(p.nlow + r);
-    const int64_t lo = r - p.h < 0 ? 0 : r - p.h, hi = r + p.h > p.n - 1 ? p.n - 1 : r + p.h;
-    b0[i] = static_cast<int32_t>(lo);
-    blen[i] = r0 + i < p.n ? static_cast<int32_t>(hi - lo + 1) : 0;
+    for (int g = 0; g < GR; ++g) {
+      const bool in = base + lane < cnt[g];
+      mc[g] = in ? __ldg(p.col + e0[g] + base + lane) : 0;
+      mv[g] = in ? F::load(p.val, e0[g] + base + lane) : zero_val(Val{});
+    }
+    const int32_t lim = maxcnt - base < 32 ? maxcnt - base : 32;
+    for (int32_t j = 0; j < lim; ++j) {
+      // no branches: every row's gathers are issued before the first MAC. A row without a j-th entry
+      // takes v = 0 (the zero fill above) and w = 0: acc + 0 * 0 == acc bit for bit (acc is never -0)
+      double2 w[GR][kCH];
+      Val v[GR];
+#pragma unroll
+      for (int g = 0; g < GR; ++g) {
+        const bool in = base + j < cnt[g];  // warp-uniform
+        const char* src = gb + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(0xffffffffu, mc[g], j))) * p.ldg_b;
+        v[g] = shfl_val(mv[g], j);
+#pragma unroll
+        for (int c = 0; c < kCH; ++c) w[g][c] = in && ok[c] ? ld_nc(src + c * 512) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int g = 0; g < GR; ++g)
+#pragma unroll
+        for (int c = 0; c < kCH; ++c) acc[g][c] = F::mac(acc[g][c], v[g], w[g][c]);
+    }
+  }
+}
+
+// One warp per (block of R consecutive rows, panel of 32 x kCH 16-byte vectors); Step mode. A CTA's
+// warps take consecutive row blocks of ONE panel (they sweep nearly the same W rows: L1 hits), and
+// consecutive CTAs take the panels of one row group (they stream the same operator values: L2 hits).
+//
+// Band sweep: the union of the R bands in chunks of KC columns. A chunk's R x KC operator values are
+// loaded coalesced one chunk AHEAD (registers), parked in the warp's shared-memory slot and read back
+// as broadcasts with compile-time offsets, so the inner loop is: one W row panel (loaded kPF columns
+// ahead), R broadcast value reads, R x kCH MACs. Chunks inside every row's band (all but the first
+// and last one or two) run without per-entry checks.
+template <class F, int R, int KC, class RP, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) cheb_band_kernel(const BArgs p) {
+  using Val = typename F::Val;
+  constexpr int NW = NT / 32;
+  constexpr int NV = R * KC / 32;  // values per lane and chunk
+  constexpr int RPJ = 32 / KC;     // rows covered by one 32-lane load
+  static_assert(KC <= 32 && 32 % KC == 0 && (R * KC) % 32 == 0 && KC % kPF == 0, "band kernel geometry");
+  __shared__ Val sm_all[NW][R * KC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Val* sm = sm_all[warp];
+  const int64_t group = blockIdx.x / p.n_panels;
+  const int panel = static_cast<int>(blockIdx.x - group * p.n_panels);
+  const int64_t r0 = (group * NW + warp) * R;
+  if (r0 >= p.n) return;  // warp-uniform; no CTA-wide barrier below
+  const uint32_t voff = (static_cast<uint32_t>(panel) * 32 * kCH + lane) * 16u;
+  bool ok[kCH];
+#pragma unroll
+  for (int c = 0; c < kCH; ++c) ok[c] = panel * 32 * kCH + c * 32 + lane < p.valid;
+  const bool full_panel = (panel + 1) * 32 * kCH <= p.valid;
+  const int32_t h = p.h;
+  const int32_t n32 = static_cast<int32_t>(p.n);
+  const int32_t rr0 = static_cast<int32_t>(r0);
+  const int32_t rows = n32 - rr0 < R ? n32 - rr0 : R;  // rows of this block that exist
+  // union of the bands: [cs, ce)
+  const int32_t cs = rr0 - h < 0 ? 0 : rr0 - h;
+  const int32_t ce = (rr0 + rows - 1 + h > n32 - 1 ? n32 - 1 : rr0 + rows - 1 + h) + 1;
+  const int32_t n_chunks = (ce - cs + KC - 1) / KC;
+  // chunks [m_lo, m_hi) lie inside every row's band and need no checks (full blocks and panels only)
+  int32_t m_lo = 0, m_hi = 0;
+  if (rows == R && full_panel) {
+    const int32_t ilo = rr0 + R - 1 - h < 0 ? 0 : rr0 + R - 1 - h;             // last row's first column
+    const int32_t ihi = (rr0 + h > n32 - 1 ? n32 - 1 : rr0 + h) + 1;           // first row's end
+    const int32_t lim = ihi < n32 - kPF ? ihi : n32 - kPF;                     // the W prefetch stays inside W
+    m_lo = (ilo - cs + KC - 1) / KC;
+    m_hi = lim - cs >= 0 ? (lim - cs) / KC : 0;
+    if (m_hi < m_lo) m_hi = m_lo;
+  }
+  // this lane's rows of a chunk load: value j is row (j RPJ + lane / KC), column k = lane % KC;
+  // vp[j] + cc addresses the entry of column cc
+  const int kl = lane % KC;
+  const Val* vp[NV];
+  int32_t vlo[NV], vhi[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int32_t r = rr0 + j * RPJ + lane / KC;
+    const int32_t rc = r < n32 ? r : n32 - 1;
+    const int32_t lo = rc - h < 0 ? 0 : rc - h;
+    vlo[j] = lo;
+    vhi[j] = r < n32 ? (rc + h > n32 - 1 ? n32 - 1 : rc + h) + 1 : lo;  // empty for rows past the end
+    vp[j] = static_cast<const Val*>(p.val) + (ld_rp<RP>(p.row_ptr, rc) + __ldg(p.nlow + rc) - lo);
   }
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const char* gb = p.g + voff;
-  double2 acc[R][CH];
+  double2 acc[R][kCH];
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int c = 0; c < CH; ++c) acc[i][c] = make_double2(0.0, 0.0);
+    for (int c = 0; c < kCH; ++c) acc[i][c] = make_double2(0.0, 0.0);
 
-  // 1. lower off-band entries, row by row (they precede the band in every row's column order)
+  // 1. lower off-band entries (they precede the band in every row's column order)
+  constexpr int GR = R < 4 ? R : 4;
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    if (r0 + i >= p.n) continue;
-    for (int64_t e = ld_rp<RP>(p.row_ptr, r0 + i); e < bs[i]; ++e) {
-      const char* src = gb + static_cast<uint64_t>(__ldg(p.col + e)) * p.ldg_b;
-      const typename F::Val v = F::load(p.val, e);
+  for (int i0 = 0; i0 < R; i0 += GR) {
+    int64_t e0[GR];
+    int32_t cnt[GR];
 #pragma unroll
-      for (int c = 0; c < CH; ++c)
-        if (ok[c]) acc[i][c] = F::mac(acc[i][c], v, ld_nc(src + c * 512));
+    for (int g = 0; g < GR; ++g) {
+      const bool ex = i0 + g < rows;
+      e0[g] = ex ? ld_rp<RP>(p.row_ptr, r0 + i0 + g) : 0;
+      cnt[g] = ex ? __ldg(p.nlow + r0 + i0 + g) : 0;
     }
+    offband<F, GR>(p, gb, ok, e0, cnt, acc + i0, lane);
   }
-  // 2. the band sweep: columns of the union of the R bands, ascending; each W row panel is loaded
-  // once (PF columns ahead) and applied to every row whose band holds the column
-  const int32_t cs = b0[0];
-  int32_t ce = b0[0] + blen[0];
+
+  // 2. the band sweep
+  auto load_chunk = [&](int32_t m, Val (&regs)[NV]) {
+    const int32_t cc = cs + m * KC + kl;
+    if (m >= m_lo && m < m_hi) {
 #pragma unroll
-  for (int i = 1; i < R; ++i) ce = blen[i] ? b0[i] + blen[i] : ce;
-  constexpr int PF = 2;
-  double2 wq[PF][CH];
+      for (int j = 0; j < NV; ++j) regs[j] = F::ldp(vp[j] + cc);
+    } else {
 #pragma unroll
-  for (int k = 0; k < PF; ++k)
+      for (int j = 0; j < NV; ++j) regs[j] = cc >= vlo[j] && cc < vhi[j] ? F::ldp(vp[j] + cc) : zero_val(Val{});
+    }
+  };
+  Val regs[NV];
+  load_chunk(0, regs);
+  double2 wq[kPF][kCH];
 #pragma unroll
-    for (int c = 0; c < CH; ++c)
+  for (int k = 0; k < kPF; ++k)
+#pragma unroll
+    for (int c = 0; c < kCH; ++c)
       wq[k][c] = ok[c] && cs + k < ce ? ld_nc(gb + static_cast<uint64_t>(cs + k) * p.ldg_b + c * 512)
                                       : make_double2(0.0, 0.0);
-  for (int32_t col = cs; col < ce; col += PF) {
+  const char* wnext = gb + static_cast<uint64_t>(cs + kPF) * p.ldg_b;  // W row of the next refill
 #pragma unroll
-    for (int k = 0; k < PF; ++k) {
-      const int32_t cc = col + k;
-      if (cc >= ce) break;
-      double2 w[CH];
+  for (int j = 0; j < NV; ++j) sm[j * 32 + lane] = regs[j];
+  __syncwarp();
+  const int32_t rmh = rr0 - h;
+  for (int32_t m = 0; m < n_chunks; ++m) {
+    if (m + 1 < n_chunks) load_chunk(m + 1, regs);
+    const int32_t c0 = cs + m * KC;
+    if (m >= m_lo && m < m_hi) {
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        w[c] = wq[k][c];
-        if (ok[c] && cc + PF < ce) wq[k][c] = ld_nc(gb + static_cast<uint64_t>(cc + PF) * p.ldg_b + c * 512);
+      for (int k = 0; k < KC; ++k) {
+        double2 w[kCH];
+#pragma unroll
+        for (int c = 0; c < kCH; ++c) {
+          w[c] = wq[k % kPF][c];
+          wq[k % kPF][c] = ld_nc(wnext + c * 512);
+        }
+        wnext += p.ldg_b;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const Val a = sm[i * KC + k];
+#pragma unroll
+          for (int c = 0; c < kCH; ++c) acc[i][c] = F::mac(acc[i][c], a, w[c]);
+        }
       }
+    } else {
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        const int32_t d = cc - b0[i];
-        if (static_cast<uint32_t>(d) < static_cast<uint32_t>(blen[i])) {
-          const typename F::Val v = F::load(p.val, bs[i] + d);
+      for (int k = 0; k < KC; ++k) {
+        const int32_t cc = c0 + k;
+        double2 w[kCH];
 #pragma unroll
-          for (int c = 0; c < CH; ++c) acc[i][c] = F::mac(acc[i][c], v, w[c]);
+        for (int c = 0; c < kCH; ++c) {
+          w[c] = wq[k % kPF][c];
+          if (ok[c] && cc + kPF < ce) wq[k % kPF][c] = ld_nc(wnext + c * 512);
+        }
+        wnext += p.ldg_b;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          // column cc is in row (r0 + i)'s band iff r0 + i - h <= cc <= r0 + i + h (cc is a valid
+          // column already) and the row exists
+          if (static_cast<uint32_t>(cc - rmh - i) <= static_cast<uint32_t>(2 * h) && i < rows && cc < ce) {
+            const Val a = sm[i * KC + k];
+#pragma unroll
+            for (int c = 0; c < kCH; ++c) acc[i][c] = F::mac(acc[i][c], a, w[c]);
+          }
         }
       }
     }
-  }
-  // 3. upper off-band entries, row by row
+    __syncwarp();
+    if (m + 1 < n_chunks) {
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    if (r0 + i >= p.n) continue;
-    const int64_t e1 = ld_rp<RP>(p.row_ptr, r0 + i + 1);
-    for (int64_t e = bs[i] + blen[i]; e < e1; ++e) {
-      const char* src = gb + static_cast<uint64_t>(__ldg(p.col + e)) * p.ldg_b;
-      const typename F::Val v = F::load(p.val, e);
-#pragma unroll
-      for (int c = 0; c < CH; ++c)
-        if (ok[c]) acc[i][c] = F::mac(acc[i][c], v, ld_nc(src + c * 512));
+      for (int j = 0; j < NV; ++j) sm[j * 32 + lane] = regs[j];
     }
+    __syncwarp();
   }
+
+  // 3. upper off-band entries
+#pragma unroll
+  for (int i0 = 0; i0 < R; i0 += GR) {
+    int64_t e0[GR];
+    int32_t cnt[GR];
+#pragma unroll
+    for (int g = 0; g < GR; ++g) {
+      const bool ex = i0 + g < rows;
+      const int64_t r = ex ? r0 + i0 + g : r0;
+      const int32_t rc = static_cast<int32_t>(r);
+      const int32_t blen = (rc + h > n32 - 1 ? n32 - 1 : rc + h) - (rc - h < 0 ? 0 : rc - h) + 1;
+      e0[g] = ld_rp<RP>(p.row_ptr, r) + __ldg(p.nlow + r) + blen;
+      cnt[g] = ex ? static_cast<int32_t>(ld_rp<RP>(p.row_ptr, r + 1) - e0[g]) : 0;
+    }
+    offband<F, GR>(p, gb, ok, e0, cnt, acc + i0, lane);
+  }
+
   // 4. epilogue: v = (((s0 aw) + (s1 w)) - v) + (s2 y)   (cheb_filter.cpp:170-171, 176-177)
   const uint64_t pol = policy_evict_first();
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int64_t r = r0 + i;
-    if (r >= p.n) continue;
+    if (i >= rows) continue;
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
+    for (int c = 0; c < kCH; ++c) {
       if (!ok[c]) continue;
       const uint32_t o = voff + c * 512;
       const double2 own = ld_nc(p.g + static_cast<uint64_t>(r) * p.ldg_b + o);
@@ -222,15 +358,16 @@ __global__ void __launch_bounds__(256, MINB) cheb_band_kernel(const BArgs p) {
   }
 }
 
-template <class F, int R, int CH, class RP, int MINB>
+template <class F, int R, int KC, class RP, int NT, int MINB>
 void launch_band(adp_ctx* ctx, BArgs k, int64_t qv) {
+  constexpr int NW = NT / 32;
   k.n_blocks = static_cast<int32_t>((k.n + R - 1) / R);
-  k.n_panels = static_cast<int32_t>((qv + 32 * CH - 1) / (32 * CH));
+  k.n_panels = static_cast<int32_t>((qv + 32 * kCH - 1) / (32 * kCH));
   k.valid = static_cast<int32_t>(qv);
-  const int64_t tasks = static_cast<int64_t>(k.n_blocks) * k.n_panels;
-  const int64_t grid = (tasks + 7) / 8;
+  const int64_t groups = (static_cast<int64_t>(k.n_blocks) + NW - 1) / NW;
+  const int64_t grid = groups * k.n_panels;
   if (grid >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_band: too many tasks");
-  launch_pdl(ctx, cheb_band_kernel<F, R, CH, RP, MINB>, dim3(static_cast<unsigned>(grid)), dim3(256), 0, k);
+  launch_pdl(ctx, cheb_band_kernel<F, R, KC, RP, NT, MINB>, dim3(static_cast<unsigned>(grid)), dim3(NT), 0, k);
   ADP_LAUNCH_CHECK();
   ctx->launches += 1;
 }
@@ -287,7 +424,7 @@ bool launch_step_band(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
   if (mode != StepMode::Step) return false;
   if (ctx->variant == 0 && !ctx->auto_band) return false;
-  if (ctx->variant != 0 && ctx->variant != 6 && ctx->variant != 7) return false;
+  if (ctx->variant != 0 && (ctx->variant < 6 || ctx->variant > 8)) return false;
   if (s.row_begin != 0 || s.row_end != a->n_rows || s.goff != 0 || s.n_push != 0) return false;
   if (a->n_rows != a->n_cols || a->nnz < 32 * a->n_rows) return false;  // long rows only (config 5: 541)
   const bool cplx = a->dtype == ADP_C128;
@@ -315,15 +452,20 @@ bool launch_step_band(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   k.s1 = s.s1;
   k.s2 = s.s2;
   const int64_t qv = (s.q + epv - 1) / epv;
-  if (ctx->variant == 7) {  // measurement: 4-row blocks (fewer registers, more resident warps)
-    if (cplx) a->rp64 ? launch_band<CplxB, 4, 2, int64_t, 2>(ctx, k, qv) : launch_band<CplxB, 4, 2, int32_t, 2>(ctx, k, qv);
-    else a->rp64 ? launch_band<RealB, 4, 2, int64_t, 2>(ctx, k, qv) : launch_band<RealB, 4, 2, int32_t, 2>(ctx, k, qv);
+  // R = 8 rows x KC = 16 columns per chunk, 6 warps per CTA, two CTAs per SM (<= 168 registers);
+  // variant 7 (measurement): R = 4 x KC = 32, 8 warps per CTA, <= 128 registers
+  if (ctx->variant == 7) {
+    if (cplx) a->rp64 ? launch_band<CplxB, 4, 32, int64_t, 256, 2>(ctx, k, qv) : launch_band<CplxB, 4, 32, int32_t, 256, 2>(ctx, k, qv);
+    else a->rp64 ? launch_band<RealB, 4, 32, int64_t, 256, 2>(ctx, k, qv) : launch_band<RealB, 4, 32, int32_t, 256, 2>(ctx, k, qv);
+  } else if (ctx->variant == 8) {  // measurement: R = 8 without the register cap (8 warps per SM)
+    if (cplx) a->rp64 ? launch_band<CplxB, 8, 16, int64_t, 256, 1>(ctx, k, qv) : launch_band<CplxB, 8, 16, int32_t, 256, 1>(ctx, k, qv);
+    else a->rp64 ? launch_band<RealB, 8, 16, int64_t, 256, 1>(ctx, k, qv) : launch_band<RealB, 8, 16, int32_t, 256, 1>(ctx, k, qv);
   } else if (cplx) {
-    if (a->rp64) launch_band<CplxB, 8, 2, int64_t, 1>(ctx, k, qv);
-    else launch_band<CplxB, 8, 2, int32_t, 1>(ctx, k, qv);
+    if (a->rp64) launch_band<CplxB, 8, 16, int64_t, 192, 2>(ctx, k, qv);
+    else launch_band<CplxB, 8, 16, int32_t, 192, 2>(ctx, k, qv);
   } else {
-    if (a->rp64) launch_band<RealB, 8, 2, int64_t, 1>(ctx, k, qv);
-    else launch_band<RealB, 8, 2, int32_t, 1>(ctx, k, qv);
+    if (a->rp64) launch_band<RealB, 8, 16, int64_t, 192, 2>(ctx, k, qv);
+    else launch_band<RealB, 8, 16, int32_t, 192, 2>(ctx, k, qv);
   }
   return true;
 }

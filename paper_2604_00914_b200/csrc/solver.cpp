@@ -31,7 +31,7 @@ struct DeviceBlock {
   int64_t ld = 0;
   DeviceBlock() = default;
   DeviceBlock(int64_t n, int64_t cols) {
-    ld = std::max<int64_t>(2, ((cols + 1) / 2) * 2);
+    ld = std::max<int64_t>(2, adp::block_ld(cols, false));
     const size_t bytes = static_cast<size_t>(std::max<int64_t>(n, 1)) * ld * 8;
     ADP_CUDA(cudaMalloc(&ptr, bytes));
     ADP_CUDA(cudaMemset(ptr, 0, bytes));

@@ -210,6 +210,15 @@ class DistributedFilter:
         return out
 
 
+def block_ld(q: int, cplx: bool = False) -> int:
+    """Leading dimension (elements) of a row-major device block of q columns, as csrc/capi.cu block_ld:
+    an even number of fp64 columns, and whole 256-byte panels for blocks wider than one panel."""
+    m = 16 if cplx else 32
+    if q > m:
+        return (q + m - 1) // m * m
+    return q if cplx else ((q + 1) // 2) * 2
+
+
 class CudaStepBackend:
     """Device backend: torch CUDA tensors + adp_step_device; halo via torch.distributed (NCCL)."""
 
@@ -227,10 +236,11 @@ class CudaStepBackend:
         return DeviceCsr(part.csr, self.ctx)
 
     def alloc(self, n, q, cplx=False):
-        if cplx:  # complex128: 16-byte elements, any width is 16-byte aligned
-            return self.torch.zeros(n, q, dtype=self.torch.complex128, device="cuda")
-        ld = ((q + 1) // 2) * 2
-        return self.torch.zeros(n, ld, dtype=self.torch.float64, device="cuda")[:, :q]
+        # row pitch as the C-ABI's own blocks (block_ld): 16-byte aligned rows, whole 256-byte panels
+        # once the block is wider than one (misaligned rows cost the sweep kernel 15-75%)
+        ld = block_ld(q, cplx)
+        dt = self.torch.complex128 if cplx else self.torch.float64
+        return self.torch.zeros(n, ld, dtype=dt, device="cuda")[:, :q]
 
     def width(self, x):
         return x.shape[1]

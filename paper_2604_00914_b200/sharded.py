@@ -217,18 +217,18 @@ class TorchOps(NumpyOps):
 
 # ---------------------------------------------------------------------------- sparse ---
 def _even_ld(x):
-    """A row-major CUDA block the step kernels accept (they move 16-byte vectors: an even row pitch for
-    fp64): x itself, or a copy with that layout viewed at x's width (torch.linalg may return
-    column-major results)."""
+    """A row-major CUDA block the step kernels accept and run fast on: x itself when its row pitch is
+    the C-ABI's block pitch (distributed.block_ld: 16-byte vectors, whole 256-byte panels for wide
+    blocks), else a copy with that layout viewed at x's width (torch.linalg may return column-major
+    results; a p = 926 block's 7408-byte rows cost the sweep kernel up to 75%)."""
     if isinstance(x, np.ndarray):
         return x
-    q = x.shape[1]
-    if x.stride(1) == 1 and x.stride(0) >= q and (x.is_complex() or x.stride(0) % 2 == 0):
-        return x
-    import torch
+    from .distributed import block_ld
 
-    buf = torch.empty(x.shape[0], q + (0 if x.is_complex() else q % 2), dtype=x.dtype, device=x.device)
-    v = buf[:, :q]
+    q = x.shape[1]
+    if x.stride(1) == 1 and x.stride(0) == block_ld(q, x.is_complex()) and x.data_ptr() % 256 == 0:
+        return x
+    v = _empty_even(x)
     v.copy_(x)
     return v
 
@@ -238,8 +238,10 @@ def _empty_even(x):
         return np.empty_like(x)
     import torch
 
-    q = x.shape[1] + (0 if x.is_complex() else x.shape[1] % 2)
-    return torch.empty(x.shape[0], q, dtype=x.dtype, device=x.device)[:, : x.shape[1]]
+    from .distributed import block_ld
+
+    ld = block_ld(x.shape[1], x.is_complex())
+    return torch.empty(x.shape[0], ld, dtype=x.dtype, device=x.device)[:, : x.shape[1]]
 
 
 class ShardSparse:

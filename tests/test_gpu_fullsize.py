@@ -137,4 +137,7 @@ def test_host_api_pipelined_chunks_equal_device_api(ctx):
                                            xr.ctypes.data_as(C.c_void_p), a.n_rows, q, q, 1,
                                            yr.ctypes.data_as(C.c_void_p), q, C.byref(cnt)))
         assert np.array_equal(yd, yr), q
-        assert cnt.value == 7 * q
+        deg = 7  # trailing exactly-zero coefficients reduce the degree (cheb_filter.cpp:141-142)
+        while deg > 0 and coeffs[deg] == 0.0:
+            deg -= 1
+        assert cnt.value == deg * q
