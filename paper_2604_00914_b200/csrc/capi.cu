@@ -372,7 +372,7 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols) {
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant) {
   return guarded([&] {
     // 0 automatic; 1-5 force one kernel family (adp.h)
-    if (variant < 0 || variant > 9) fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
+    if (variant < 0 || variant > 11) fail(ADP_ERR_CONFIG, "adp_ctx_set_tuning: unknown variant");
     ctx->variant = variant;
   });
 }

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -120,13 +121,39 @@ __device__ __forceinline__ double2 zero_val(double2) { return make_double2(0.0, 
 // Off-band entries [e0, e0 + cnt) of GR consecutive rows (warp-uniform e0 / cnt per row), entry by
 // entry in CSR order per row, the GR rows interleaved so GR x kCH gathers are in flight. Columns and
 // values are fetched 32 entries at a time (coalesced) and handed out by shuffles.
-template <class F, int GR>
-__device__ __forceinline__ void offband(const BArgs& p, const char* gb, const bool (&ok)[kCH], const int64_t (&e0)[GR],
-                                        const int32_t (&cnt)[GR], double2 (*acc)[kCH], int lane) {
+
+// 16-byte asynchronous copy global -> shared, bypassing L1 (the gathered rows are used once);
+// bytes = 0 writes zeros without reading.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const char* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ double2 lds128(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+
+// Off-band entries [e0, e0 + cnt) of GR consecutive rows (warp-uniform e0 / cnt per row), entry by
+// entry in CSR order per row, the GR rows interleaved. Columns and values are fetched 32 entries at a
+// time (coalesced) and handed out by shuffles. The gathered W row panels are random rows of a block
+// far larger than L2 -- each a DRAM round trip -- so they land through a ring of D stages of
+// asynchronous copies in the warp's shared-memory slot (each lane copies and reads back its own 16
+// bytes: no cross-lane ordering): D x GR row panels are in flight per warp without holding registers,
+// and the gathers bypass L1, which keeps the band's W rows.
+template <class F, int GR, int D>
+__device__ __forceinline__ void offband(const BArgs& p, const char* gb, uint32_t ring,
+                                        const bool (&ok)[kCH], const int64_t (&e0)[GR], const int32_t (&cnt)[GR],
+                                        double2 (*acc)[kCH], int lane) {
   using Val = typename F::Val;
   int32_t maxcnt = 0;
 #pragma unroll
   for (int g = 0; g < GR; ++g) maxcnt = cnt[g] > maxcnt ? cnt[g] : maxcnt;
+  constexpr uint32_t kStage = GR * kCH * 512;        // bytes of one ring stage
   for (int32_t base = 0; base < maxcnt; base += 32) {
     int32_t mc[GR];
     Val mv[GR];
@@ -137,26 +164,48 @@ __device__ __forceinline__ void offband(const BArgs& p, const char* gb, const bo
       mv[g] = in ? F::load(p.val, e0[g] + base + lane) : zero_val(Val{});
     }
     const int32_t lim = maxcnt - base < 32 ? maxcnt - base : 32;
+    auto issue = [&](int32_t j) {  // entry j of every row -> stage j % D (zeros where a row has no j-th entry)
+      const uint32_t dst = ring + static_cast<uint32_t>(j % D) * kStage + lane * 16;
+#pragma unroll
+      for (int g = 0; g < GR; ++g) {
+        const bool in = j < 32 && base + j < cnt[g];  // warp-uniform
+        const char* src = gb + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(0xffffffffu, mc[g], j & 31))) * p.ldg_b;
+#pragma unroll
+        for (int c = 0; c < kCH; ++c) cp_async16(dst + (g * kCH + c) * 512, src + c * 512, in && ok[c] ? 16u : 0u);
+      }
+      cp_async_commit();
+    };
+#pragma unroll 1
+    for (int t = 0; t < D - 1; ++t) issue(t);
+#pragma unroll 1
     for (int32_t j = 0; j < lim; ++j) {
-      // no branches: every row's gathers are issued before the first MAC. A row without a j-th entry
-      // takes v = 0 (the zero fill above) and w = 0: acc + 0 * 0 == acc bit for bit (acc is never -0)
+      issue(j + D - 1);  // stage (j - 1) % D: its reads finished with iteration j - 1's MACs
+      cp_async_wait<D - 1>();
+      // A row without a j-th entry takes v = 0 (the zero fill above) and w = 0 (zero-filled copy):
+      // acc + 0 * 0 == acc bit for bit (acc is never -0)
+      const uint32_t st = ring + static_cast<uint32_t>(j % D) * kStage + lane * 16;
       double2 w[GR][kCH];
       Val v[GR];
 #pragma unroll
       for (int g = 0; g < GR; ++g) {
-        const bool in = base + j < cnt[g];  // warp-uniform
-        const char* src = gb + static_cast<uint64_t>(static_cast<uint32_t>(__shfl_sync(0xffffffffu, mc[g], j))) * p.ldg_b;
         v[g] = shfl_val(mv[g], j);
 #pragma unroll
-        for (int c = 0; c < kCH; ++c) w[g][c] = in && ok[c] ? ld_nc(src + c * 512) : make_double2(0.0, 0.0);
+        for (int c = 0; c < kCH; ++c) w[g][c] = lds128(st + (g * kCH + c) * 512);
       }
 #pragma unroll
       for (int g = 0; g < GR; ++g)
 #pragma unroll
         for (int c = 0; c < kCH; ++c) acc[g][c] = F::mac(acc[g][c], v[g], w[g][c]);
     }
+    cp_async_wait<0>();
   }
 }
+
+template <class F, int R, int KC, int GR, int D>
+struct BandSlot {
+  static constexpr uint32_t ring = D * GR * kCH * 512, vals = R * KC * sizeof(typename F::Val);
+  static constexpr uint32_t bytes = ring > vals ? ring : vals;
+};
 
 // One warp per (block of R consecutive rows, panel of 32 x kCH 16-byte vectors); Step mode. A CTA's
 // warps take consecutive row blocks of ONE panel (they sweep nearly the same W rows: L1 hits), and
@@ -167,16 +216,20 @@ __device__ __forceinline__ void offband(const BArgs& p, const char* gb, const bo
 // as broadcasts with compile-time offsets, so the inner loop is: one W row panel (loaded kPF columns
 // ahead), R broadcast value reads, R x kCH MACs. Chunks inside every row's band (all but the first
 // and last one or two) run without per-entry checks.
-template <class F, int R, int KC, class RP, int NT, int MINB>
+template <class F, int R, int KC, class RP, int NT, int MINB, int GR, int D>
 __global__ void __launch_bounds__(NT, MINB) cheb_band_kernel(const BArgs p) {
   using Val = typename F::Val;
+  static_assert(R % GR == 0 && D >= 2, "band kernel gather geometry");
   constexpr int NW = NT / 32;
   constexpr int NV = R * KC / 32;  // values per lane and chunk
   constexpr int RPJ = 32 / KC;     // rows covered by one 32-lane load
   static_assert(KC <= 32 && 32 % KC == 0 && (R * KC) % 32 == 0 && KC % kPF == 0, "band kernel geometry");
-  __shared__ Val sm_all[NW][R * KC];
+  // per warp: the gather ring (off-band phases), reused as the value chunk slot (band sweep)
+  constexpr uint32_t kSlot = BandSlot<F, R, KC, GR, D>::bytes;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Val* sm = sm_all[warp];
+  Val* sm = reinterpret_cast<Val*>(smem_raw + warp * kSlot);
+  const uint32_t ring = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
   const int64_t group = blockIdx.x / p.n_panels;
   const int panel = static_cast<int>(blockIdx.x - group * p.n_panels);
   const int64_t r0 = (group * NW + warp) * R;
@@ -227,8 +280,11 @@ __global__ void __launch_bounds__(NT, MINB) cheb_band_kernel(const BArgs p) {
 #pragma unroll
     for (int c = 0; c < kCH; ++c) acc[i][c] = make_double2(0.0, 0.0);
 
-  // 1. lower off-band entries (they precede the band in every row's column order)
-  constexpr int GR = R < 4 ? R : 4;
+  // Phases: 0 = lower off-band entries (they precede the band in every row's column order) and the
+  // band sweep, 1 = upper off-band entries. One loop so the gather code exists once (the kernel must
+  // stay inside the instruction cache: three warps per scheduler sit at different phases).
+#pragma unroll 1
+  for (int phase = 0; phase < 2; ++phase) {
 #pragma unroll
   for (int i0 = 0; i0 < R; i0 += GR) {
     int64_t e0[GR];
@@ -236,11 +292,17 @@ __global__ void __launch_bounds__(NT, MINB) cheb_band_kernel(const BArgs p) {
 #pragma unroll
     for (int g = 0; g < GR; ++g) {
       const bool ex = i0 + g < rows;
-      e0[g] = ex ? ld_rp<RP>(p.row_ptr, r0 + i0 + g) : 0;
-      cnt[g] = ex ? __ldg(p.nlow + r0 + i0 + g) : 0;
+      const int64_t r = ex ? r0 + i0 + g : r0;
+      const int32_t rc = static_cast<int32_t>(r);
+      const int32_t blen = (rc + h > n32 - 1 ? n32 - 1 : rc + h) - (rc - h < 0 ? 0 : rc - h) + 1;
+      const int64_t rb = ld_rp<RP>(p.row_ptr, r);
+      const int32_t nl = __ldg(p.nlow + r);
+      e0[g] = phase == 0 ? rb : rb + nl + blen;
+      cnt[g] = !ex ? 0 : (phase == 0 ? nl : static_cast<int32_t>(ld_rp<RP>(p.row_ptr, r + 1) - e0[g]));
     }
-    offband<F, GR>(p, gb, ok, e0, cnt, acc + i0, lane);
+    offband<F, GR, D>(p, gb, ring, ok, e0, cnt, acc + i0, lane);
   }
+  if (phase == 1) break;
 
   // 2. the band sweep
   auto load_chunk = [&](int32_t m, Val (&regs)[NV]) {
@@ -271,41 +333,49 @@ __global__ void __launch_bounds__(NT, MINB) cheb_band_kernel(const BArgs p) {
     if (m + 1 < n_chunks) load_chunk(m + 1, regs);
     const int32_t c0 = cs + m * KC;
     if (m >= m_lo && m < m_hi) {
+      constexpr int UK = KC < 8 ? KC : 8;  // columns per unrolled body (code size: the loop must stay in the instruction cache)
+#pragma unroll 1
+      for (int k0 = 0; k0 < KC; k0 += UK) {
+        const Val* smk = sm + k0;
 #pragma unroll
-      for (int k = 0; k < KC; ++k) {
-        double2 w[kCH];
+        for (int k = 0; k < UK; ++k) {
+          double2 w[kCH];
 #pragma unroll
-        for (int c = 0; c < kCH; ++c) {
-          w[c] = wq[k % kPF][c];
-          wq[k % kPF][c] = ld_nc(wnext + c * 512);
-        }
-        wnext += p.ldg_b;
+          for (int c = 0; c < kCH; ++c) {
+            w[c] = wq[k % kPF][c];
+            wq[k % kPF][c] = ld_nc(wnext + c * 512);
+          }
+          wnext += p.ldg_b;
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const Val a = sm[i * KC + k];
+          for (int i = 0; i < R; ++i) {
+            const Val a = smk[i * KC + k];
 #pragma unroll
-          for (int c = 0; c < kCH; ++c) acc[i][c] = F::mac(acc[i][c], a, w[c]);
+            for (int c = 0; c < kCH; ++c) acc[i][c] = F::mac(acc[i][c], a, w[c]);
+          }
         }
       }
     } else {
+#pragma unroll 1
+      for (int k0 = 0; k0 < KC; k0 += kPF) {
 #pragma unroll
-      for (int k = 0; k < KC; ++k) {
-        const int32_t cc = c0 + k;
-        double2 w[kCH];
+        for (int k = 0; k < kPF; ++k) {
+          const int32_t cc = c0 + k0 + k;
+          double2 w[kCH];
 #pragma unroll
-        for (int c = 0; c < kCH; ++c) {
-          w[c] = wq[k % kPF][c];
-          if (ok[c] && cc + kPF < ce) wq[k % kPF][c] = ld_nc(wnext + c * 512);
-        }
-        wnext += p.ldg_b;
+          for (int c = 0; c < kCH; ++c) {
+            w[c] = wq[k][c];
+            if (ok[c] && cc + kPF < ce) wq[k][c] = ld_nc(wnext + c * 512);
+          }
+          wnext += p.ldg_b;
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-          // column cc is in row (r0 + i)'s band iff r0 + i - h <= cc <= r0 + i + h (cc is a valid
-          // column already) and the row exists
-          if (static_cast<uint32_t>(cc - rmh - i) <= static_cast<uint32_t>(2 * h) && i < rows && cc < ce) {
-            const Val a = sm[i * KC + k];
+          for (int i = 0; i < R; ++i) {
+            // column cc is in row (r0 + i)'s band iff r0 + i - h <= cc <= r0 + i + h (cc is a valid
+            // column already) and the row exists
+            if (static_cast<uint32_t>(cc - rmh - i) <= static_cast<uint32_t>(2 * h) && i < rows && cc < ce) {
+              const Val a = sm[i * KC + k0 + k];
 #pragma unroll
-            for (int c = 0; c < kCH; ++c) acc[i][c] = F::mac(acc[i][c], a, w[c]);
+              for (int c = 0; c < kCH; ++c) acc[i][c] = F::mac(acc[i][c], a, w[c]);
+            }
           }
         }
       }
@@ -318,22 +388,7 @@ __global__ void __launch_bounds__(NT, MINB) cheb_band_kernel(const BArgs p) {
     __syncwarp();
   }
 
-  // 3. upper off-band entries
-#pragma unroll
-  for (int i0 = 0; i0 < R; i0 += GR) {
-    int64_t e0[GR];
-    int32_t cnt[GR];
-#pragma unroll
-    for (int g = 0; g < GR; ++g) {
-      const bool ex = i0 + g < rows;
-      const int64_t r = ex ? r0 + i0 + g : r0;
-      const int32_t rc = static_cast<int32_t>(r);
-      const int32_t blen = (rc + h > n32 - 1 ? n32 - 1 : rc + h) - (rc - h < 0 ? 0 : rc - h) + 1;
-      e0[g] = ld_rp<RP>(p.row_ptr, r) + __ldg(p.nlow + r) + blen;
-      cnt[g] = ex ? static_cast<int32_t>(ld_rp<RP>(p.row_ptr, r + 1) - e0[g]) : 0;
-    }
-    offband<F, GR>(p, gb, ok, e0, cnt, acc + i0, lane);
-  }
+  }  // phases
 
   // 4. epilogue: v = (((s0 aw) + (s1 w)) - v) + (s2 y)   (cheb_filter.cpp:170-171, 176-177)
   const uint64_t pol = policy_evict_first();
@@ -358,7 +413,7 @@ __global__ void __launch_bounds__(NT, MINB) cheb_band_kernel(const BArgs p) {
   }
 }
 
-template <class F, int R, int KC, class RP, int NT, int MINB>
+template <class F, int R, int KC, class RP, int NT, int MINB, int GR, int D>
 void launch_band(adp_ctx* ctx, BArgs k, int64_t qv) {
   constexpr int NW = NT / 32;
   k.n_blocks = static_cast<int32_t>((k.n + R - 1) / R);
@@ -367,7 +422,11 @@ void launch_band(adp_ctx* ctx, BArgs k, int64_t qv) {
   const int64_t groups = (static_cast<int64_t>(k.n_blocks) + NW - 1) / NW;
   const int64_t grid = groups * k.n_panels;
   if (grid >= (int64_t{1} << 31)) fail(ADP_ERR_DIMENSION, "cheb_band: too many tasks");
-  launch_pdl(ctx, cheb_band_kernel<F, R, KC, RP, NT, MINB>, dim3(static_cast<unsigned>(grid)), dim3(NT), 0, k);
+  auto kern = cheb_band_kernel<F, R, KC, RP, NT, MINB, GR, D>;
+  constexpr size_t smem = static_cast<size_t>(NW) * BandSlot<F, R, KC, GR, D>::bytes;
+  static_assert(smem * MINB <= 200 * 1024, "band kernel shared memory");
+  ADP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  launch_pdl(ctx, kern, dim3(static_cast<unsigned>(grid)), dim3(NT), smem, k);
   ADP_LAUNCH_CHECK();
   ctx->launches += 1;
 }
@@ -424,7 +483,7 @@ bool launch_step_band(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   const adp_csr* a = s.a;
   if (mode != StepMode::Step) return false;
   if (ctx->variant == 0 && !ctx->auto_band) return false;
-  if (ctx->variant != 0 && (ctx->variant < 6 || ctx->variant > 8)) return false;
+  if (ctx->variant != 0 && (ctx->variant < 6 || ctx->variant > 11)) return false;
   if (s.row_begin != 0 || s.row_end != a->n_rows || s.goff != 0 || s.n_push != 0) return false;
   if (a->n_rows != a->n_cols || a->nnz < 32 * a->n_rows) return false;  // long rows only (config 5: 541)
   const bool cplx = a->dtype == ADP_C128;
@@ -452,21 +511,24 @@ bool launch_step_band(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   k.s1 = s.s1;
   k.s2 = s.s2;
   const int64_t qv = (s.q + epv - 1) / epv;
-  // R = 8 rows x KC = 16 columns per chunk, 6 warps per CTA, two CTAs per SM (<= 168 registers);
-  // variant 7 (measurement): R = 4 x KC = 32, 8 warps per CTA, <= 128 registers
-  if (ctx->variant == 7) {
-    if (cplx) a->rp64 ? launch_band<CplxB, 4, 32, int64_t, 256, 2>(ctx, k, qv) : launch_band<CplxB, 4, 32, int32_t, 256, 2>(ctx, k, qv);
-    else a->rp64 ? launch_band<RealB, 4, 32, int64_t, 256, 2>(ctx, k, qv) : launch_band<RealB, 4, 32, int32_t, 256, 2>(ctx, k, qv);
-  } else if (ctx->variant == 8) {  // measurement: R = 8 without the register cap (8 warps per SM)
-    if (cplx) a->rp64 ? launch_band<CplxB, 8, 16, int64_t, 256, 1>(ctx, k, qv) : launch_band<CplxB, 8, 16, int32_t, 256, 1>(ctx, k, qv);
-    else a->rp64 ? launch_band<RealB, 8, 16, int64_t, 256, 1>(ctx, k, qv) : launch_band<RealB, 8, 16, int32_t, 256, 1>(ctx, k, qv);
-  } else if (cplx) {
-    if (a->rp64) launch_band<CplxB, 8, 16, int64_t, 192, 2>(ctx, k, qv);
-    else launch_band<CplxB, 8, 16, int32_t, 192, 2>(ctx, k, qv);
-  } else {
-    if (a->rp64) launch_band<RealB, 8, 16, int64_t, 192, 2>(ctx, k, qv);
-    else launch_band<RealB, 8, 16, int32_t, 192, 2>(ctx, k, qv);
+  // geometry (rows per warp R, columns per value chunk KC, threads per CTA, CTAs per SM); the automatic
+  // choice is variant 6's, variants 7-11 are measurement alternatives
+#define ADP_BAND(R_, KC_, NT_, MB_, GR_, D_)                                                                     \
+  do {                                                                                                           \
+    if (cplx) a->rp64 ? launch_band<CplxB, R_, KC_, int64_t, NT_, MB_, GR_, D_>(ctx, k, qv)                       \
+                      : launch_band<CplxB, R_, KC_, int32_t, NT_, MB_, GR_, D_>(ctx, k, qv);                      \
+    else a->rp64 ? launch_band<RealB, R_, KC_, int64_t, NT_, MB_, GR_, D_>(ctx, k, qv)                            \
+                 : launch_band<RealB, R_, KC_, int32_t, NT_, MB_, GR_, D_>(ctx, k, qv);                           \
+  } while (0)
+  switch (ctx->variant) {
+    case 7: ADP_BAND(4, 32, 256, 2, 4, 2); break;
+    case 8: ADP_BAND(4, 32, 256, 2, 2, 4); break;
+    case 9: ADP_BAND(6, 16, 256, 2, 3, 2); break;
+    case 10: ADP_BAND(4, 32, 256, 2, 4, 3); break;
+    case 11: ADP_BAND(8, 16, 128, 3, 4, 2); break;
+    default: ADP_BAND(8, 16, 192, 2, 4, 2); break;
   }
+#undef ADP_BAND
   return true;
 }
 

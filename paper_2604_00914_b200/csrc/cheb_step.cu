@@ -394,7 +394,7 @@ void launch_step_impl(adp_ctx* ctx, StepMode mode, const StepArgs& s) {
   // >= 4 vectors; this file's narrow-group row kernel for 1-3 vectors and variant 1.
   const int v = ctx->variant;
   if ((v == 0 || v == 5) && launch_step_sweep(ctx, mode, s)) return void(ctx->last_kernel = 5);
-  if ((v == 0 || (v >= 6 && v <= 8)) && launch_step_band(ctx, mode, s)) return void(ctx->last_kernel = 6);
+  if ((v == 0 || (v >= 6 && v <= 11)) && launch_step_band(ctx, mode, s)) return void(ctx->last_kernel = 6);
   if (v == 4 && launch_step_cube(ctx, mode, s)) return void(ctx->last_kernel = 4);
   if ((v == 0 || v == 3) && launch_step_line(ctx, mode, s)) return void(ctx->last_kernel = 3);
   if (v != 1 && launch_step_lean(ctx, mode, s)) return void(ctx->last_kernel = 2);

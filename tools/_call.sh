@@ -1,5 +1,6 @@
 set -u
 mkdir -p gpurun_out
-for v in 0 7; do
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:cheb_band_kernel -s 2 -c 1 -f -o gpurun_out/band_v$v python tools/c5_full.py --n 600000 --degree 4 --reps 1 --variant $v --out '' > gpurun_out/ncu_band_v$v.log 2>&1; tail -2 gpurun_out/ncu_band_v$v.log | cut -c1-300
-done
+timeout 900 python -m pytest tests/test_gpu_band.py -x -q > gpurun_out/band_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/band_tests.log
+tail -2 gpurun_out/band_tests.log
+for v in 6 7 9 11; do timeout 600 python tools/c5_full.py --variant $v --reps 2 --out gpurun_out/c5_full_v$v.json > gpurun_out/c5_v$v.log 2>&1; python -c "
+import json; d=json.load(open('gpurun_out/c5_full_v$v.json')); print('variant $v', d['ms_per_degree_step'], d['fp64_tflops'], d['fp64_frac_of_dfma_peak'], d['step_kernel'], d['clocks'])"; done
