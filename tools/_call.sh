@@ -1,6 +1,12 @@
 set -u
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_band.py -x -q > gpurun_out/band_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/band_tests.log
-tail -2 gpurun_out/band_tests.log
-for v in 6 7 9 11; do timeout 600 python tools/c5_full.py --variant $v --reps 2 --out gpurun_out/c5_full_v$v.json > gpurun_out/c5_v$v.log 2>&1; python -c "
-import json; d=json.load(open('gpurun_out/c5_full_v$v.json')); print('variant $v', d['ms_per_degree_step'], d['fp64_tflops'], d['fp64_frac_of_dfma_peak'], d['step_kernel'], d['clocks'])"; done
+timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
+tail -3 gpurun_out/gpu_tests.log
+timeout 1500 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?"
+grep '"metric"' gpurun_out/bench_full.log | tail -1 > gpurun_out/bench_full.json
+python - <<'P'
+import json
+d=json.load(open('gpurun_out/bench_full.json'))
+print(d['value'], d['roofline']['frac'], d['roofline']['launch_ms'], d['e2e']['value'], d['clocks'])
+for k,v in d['configs'].items(): print(k, v['step_launch_ms'], v.get('frac_of_hbm_peak'), v.get('frac_of_fp64_peak'), v.get('frac_of_serial_bound'))
+P
