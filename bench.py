@@ -49,7 +49,7 @@ METRIC = "Chebyshev-filter SpMM effective HBM GB/s (% of peak); end-to-end solve
 KERNELS = {1: "cheb_step_kernel (csrc/cheb_step.cu)", 2: "cheb_lean_kernel (csrc/cheb_lean.cu)",
            3: "cheb_line_kernel (csrc/cheb_line.cu)", 4: "cheb_cube_kernel (csrc/cheb_cube.cu)",
            5: "cheb_sweep_kernel (csrc/cheb_sweep.cu: plane-sweep stencil, 4-D TMA halo tiles)",
-           6: "cheb_band_kernel (csrc/cheb_band.cu: band-block sweep, W row panels shared by 8 rows)"}
+           6: "cheb_band_kernel (csrc/cheb_band.cu: band-block sweep, W row panels shared by 8 rows, cp.async gather ring)"}
 
 
 def parse_args():
@@ -387,8 +387,21 @@ def secondary(adp, configs, device, peak, fpk):
             d["fp64_tflops"] = round(flops / (launch_ms * 1e-3) / 1e12, 2)
             d["fp64_peak_tflops"], d["fp64_peak_source"] = fpk
             d["frac_of_fp64_peak"] = round(d["fp64_tflops"] / fpk[0], 4)
-            d["note"] = ("complex MAC = 4 DFMA (8 flops); bound = max(FP64, gather-inflated HBM): ~40 random off-band "
-                         "W rows per output row miss L2 (DESIGN.md 3.1)")
+            # DRAM traffic model (ncu on c5s: within 4% of it): the streamed algorithmic bytes plus one W row
+            # panel per off-band entry -- random rows of a 24.6 GB block, far beyond L2, so each is a DRAM read
+            # (band rows are read once and shared through L1 / L2)
+            n_off = nnz - n * 501 + 250 * 251  # entries outside the band (edge rows' bands are truncated)
+            dram = b_step + n_off * q * es
+            d["dram_model_bytes_per_step"] = int(dram)
+            d["dram_model_gbs"] = round(dram / (launch_ms * 1e-3) / 1e9, 1)
+            d["frac_of_hbm_peak_with_gathers"] = round(d["dram_model_gbs"] / peak, 4)
+            serial_ms = flops / (fpk[0] * 1e9) + dram / (peak * 1e6)
+            d["serial_bound_ms"] = round(serial_ms, 1)
+            d["frac_of_serial_bound"] = round(serial_ms / launch_ms, 4)
+            d["note"] = ("complex MAC = 4 DFMA (8 flops). Two resources bound this step: the FP64 pipe (flops / measured "
+                         "DFMA peak) and DRAM (streams + ~40 random off-band W row panels per row, 1.1 TB). Each peak "
+                         "was measured alone at ~1 kW; under the 1 kW cap they cannot both run at peak, so the step "
+                         "is compared with their sum (serial_bound_ms) as well as with each alone")
         out[name] = d
         del x, y
         da.close()
