@@ -83,9 +83,11 @@ adp_status adp_ctx_set_panel(adp_ctx* ctx, int32_t panel_cols);
  * (runs shared by 2-D/3-D blocks of grid lines), 5 plane-sweep stencil kernel
  * (constant-coefficient 3-D stencils: halo tiles of W streamed plane by plane
  * through shared memory), 6 band-block kernel (banded operators with sparse
- * off-band entries: W row panels shared by 8 consecutive rows), 7 the same with
- * 4-row blocks. A family that does not apply to an operator falls back to the
- * next one. Other values fail with ADP_ERR_CONFIG. */
+ * off-band entries: W row panels shared by 8 consecutive rows, off-band rows
+ * gathered through a cp.async ring), 7-11 the same with other block geometries
+ * (4 / 6 / 8 rows, ring depths 2-4; measurement alternatives). A family that
+ * does not apply to an operator falls back to the next one. Other values fail
+ * with ADP_ERR_CONFIG. */
 adp_status adp_ctx_set_tuning(adp_ctx* ctx, int32_t variant);
 
 /* -------------------------------------------------------------- operator -- */

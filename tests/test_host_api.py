@@ -189,3 +189,14 @@ def test_config5_device_generator_structure():
     assert 0.8 * 2 * off * n < (~band).sum() <= 2 * off * n
     a = adp.CsrMatrix(n, n, rp, ci, v)  # the host CsrMatrix invariant holds too
     assert a.nnz == len(v)
+
+
+def test_block_ld_matches_library():
+    # the Python row pitch of device blocks (distributed.block_ld) is the C-ABI's own (csrc/capi.cu
+    # block_ld): 16-byte rows for narrow blocks, whole 256-byte panels beyond one panel
+    from paper_2604_00914_b200.distributed import block_ld
+
+    for q, want in ((1, 2), (2, 2), (7, 8), (32, 32), (33, 64), (64, 64), (926, 928), (1000, 1024), (1024, 1024)):
+        assert block_ld(q, False) == want, q
+    for q, want in ((1, 1), (5, 5), (16, 16), (17, 32), (384, 384), (543, 544)):
+        assert block_ld(q, True) == want, q

@@ -1,12 +1,6 @@
 set -u
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
-tail -3 gpurun_out/gpu_tests.log
-timeout 1500 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?"
-grep '"metric"' gpurun_out/bench_full.log | tail -1 > gpurun_out/bench_full.json
-python - <<'P'
-import json
-d=json.load(open('gpurun_out/bench_full.json'))
-print(d['value'], d['roofline']['frac'], d['roofline']['launch_ms'], d['e2e']['value'], d['clocks'])
-for k,v in d['configs'].items(): print(k, v['step_launch_ms'], v.get('frac_of_hbm_peak'), v.get('frac_of_fp64_peak'), v.get('frac_of_serial_bound'))
-P
+timeout 3000 python tools/solve_config.py c4w --json gpurun_out/solve_c4w.json > gpurun_out/solve_c4w.txt 2>&1; echo "c4w rc=$?"
+head -3 gpurun_out/solve_c4w.txt
+timeout 4800 python tools/solve_complex.py c3 --json gpurun_out/solve_c3.json > gpurun_out/solve_c3.txt 2>&1; echo "c3 rc=$?"
+head -4 gpurun_out/solve_c3.txt | cut -c1-400
