@@ -405,3 +405,38 @@ def test_device_created_operator_validation(ctx):
         adp.DeviceCsr.from_device(4, 4, rp, ci.to(torch.int64), v, ctx=ctx)
     with pytest.raises(adp.DimensionError):
         adp.DeviceCsr.from_device(5, 5, rp, ci, v, ctx=ctx)
+
+
+def test_gpu_bitwise_vs_reference_sources(ctx, orc, golden_dir):
+    # The GPU path against the REFERENCE's own clenshaw_apply / maspmm source text (oracle/_ref: compiled
+    # from /root/reference against the Eigen stand-in, prebuilt on this box), not only against the oracle
+    # restatement: random operators, the reference's .mtx fixtures, a 7-point stencil (plane-sweep kernel).
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2604_00914_b200 import configs
+
+    rng = np.random.default_rng(11)
+    ops = [orc.random_symmetric(300, 0.04, 5), orc.random_symmetric(1025, 0.004, 6)]
+    for name in ("arrow_ints", "banded_mixed", "laplacian2d_30"):
+        z = np.load(f"{golden_dir}/fixture_{name}.npz")
+        if int(z["n_rows"]) == int(z["n_cols"]):
+            ops.append(orc.Csr(int(z["n_rows"]), int(z["n_cols"]), z["row_ptr"], z["col_idx"], z["values"]))
+    s = configs.laplacian7_potential(12, -2.0, 2.0, seed=3)
+    ops.append(orc.Csr(s.n_rows, s.n_cols, s.row_ptr, s.col_idx, s.values))
+    for a in ops:
+        bound = float(np.abs(a.to_dense()).sum(axis=1).max()) + 0.5
+        f = adp.build_filter(-0.3 * bound, 0.1 * bound, (-bound, bound), 48, 0.5)
+        coeffs, l1, l2, _, _ = ref.build_filter(-0.3 * bound, 0.1 * bound, (-bound, bound), 48, 0.5)
+        assert np.array_equal(f.coeff_array(), coeffs) and (f.l1, f.l2) == (l1, l2)
+        da = dev(ctx, a)
+        for q in (1, 7, 64, 96):
+            x = rng.standard_normal((a.n_rows, q))
+            for degree in (1, 2, 9, 48):
+                got = adp.clenshaw_apply(f, da, x, degree)
+                want, _ = ref.clenshaw_apply(coeffs, 48, l1, l2, a, 256, 64, x, degree)
+                assert_bitwise(got, want)
+            b = rng.standard_normal((a.n_cols, q))
+            assert_bitwise(adp.maspmm(da, b), ref.maspmm(a, 256, 64, b))
+        da.close()
