@@ -2,9 +2,12 @@
 // oracle/oracle.cpp -- TEST INFRASTRUCTURE ONLY.
 //
 // CPU restatement of the AdaPolySI Chebyshev-filter hot path of the reference
-// (/root/reference/proj, C++20 + Eigen + OpenMP). The reference itself cannot
-// be compiled in this image (Eigen3 and vendor/ are absent),
-// so this file restates, op for op, the functions on the path. It is the
+// (/root/reference/proj, C++20 + Eigen + OpenMP). The reference as a whole
+// cannot be compiled in this image (Eigen3 and vendor/ are absent, SURVEY.md
+// 0.4), so this file restates, op for op, the functions on the path; the
+// reference's own FILTER-PATH sources are compiled in place against a minimal
+// Eigen stand-in into oracle/_ref (ref_capi.cpp, eigen_standin/), and
+// tests/test_ref_build.py checks this restatement bit for bit against them. It is the
 // CHECKER for the CUDA product path: only tests/, __graft_entry__.smoke() and
 // bench.py's cpu_baseline / --impl reference legs may load it.
 //
