@@ -193,24 +193,41 @@ def library_mapped() -> bool:
 
 
 # ------------------------------------------------------------- CPU legs ---
+_TILED = {}
+CPU_WHAT = {"reference": "oracle/_ref: the reference's own csr_to_tiled + maspmm compiled from its sources,",
+            "port": "oracle maspmm"}
+
+
 def cpu_sample(a_csr, q: int, target_seconds: float):
-    """Degree steps of the oracle (the reference's CPU path restated) on all host threads, on ONE
-    column panel of min(q, 64) columns; returns (seconds per degree step at width q, steps, threads,
-    panels): the panel time x ceil(q / 64) -- maspmm's outer loop runs column blocks of T_k = 64
-    independently (tiled_matrix.hpp:194) and the array update is per element."""
+    """Degree steps of the reference's CPU path on all host threads, on ONE column panel of min(q, 64)
+    columns; returns (seconds per degree step at width q, steps, threads, panels, sample seconds, kind):
+    the panel time x ceil(q / 64) -- maspmm's outer loop runs column blocks of T_k = 64 independently
+    (tiled_matrix.hpp:194) and the array update is per element. kind "reference": oracle/_ref, the
+    reference's own csr_to_tiled + maspmm compiled from its sources (present when the repo was built
+    beside /root/reference; it travels prebuilt); "port": the oracle restatement (bit-identical to it,
+    tests/test_ref_build.py)."""
     from oracle import oracle as orc
+    from oracle import ref
 
     orc.build()
     threads = orc.max_threads()
     orc.set_threads(threads)
     oa = orc.Csr(a_csr.n_rows, a_csr.n_cols, a_csr.row_ptr, a_csr.col_idx, a_csr.values)
-    t = orc.Tiled(oa, 256, 64)
     qs = min(q, 64)
     panels = -(-q // 64)
-    sec1, _ = orc.bench_clenshaw_steps(t, qs, 1)  # includes first-touch; calibrates the sample size
+    key = (id(a_csr), "ref" if ref.available() else "port")
+    if key not in _TILED:  # tile once per operator (csr_to_tiled of config 4 takes seconds)
+        _TILED.clear()
+        _TILED[key] = ref.Tiled(oa, 256, 64) if ref.available() else orc.Tiled(oa, 256, 64)
+    t = _TILED[key]
+    if ref.available():
+        kind, run = "reference", (lambda steps: ref.bench_clenshaw_steps(t, qs, steps))
+    else:
+        kind, run = "port", (lambda steps: orc.bench_clenshaw_steps(t, qs, steps))
+    sec1, _ = run(1)  # includes first touch; calibrates the sample size
     steps = max(1, min(400, int(target_seconds / max(sec1, 1e-6))))
-    sec, _ = orc.bench_clenshaw_steps(t, qs, steps)
-    return sec / steps * panels, steps, threads, panels, sec
+    sec, _ = run(steps)
+    return sec / steps * panels, steps, threads, panels, sec, kind
 
 
 def run_reference(args):
@@ -235,7 +252,7 @@ def run_reference(args):
     per = max(args.cpu_seconds / max(args.steps, 1), 2.0)
     t_all = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        sec_step, steps, threads, panels, sec = cpu_sample(a, q, per if i >= args.warmup else 0.5)
+        sec_step, steps, threads, panels, sec, kind = cpu_sample(a, q, per if i >= args.warmup else 0.5)
         if i >= args.warmup:
             vals.append(b / sec_step / 1e9)
             secs.append(sec)
@@ -246,8 +263,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload(args.config, cfg, n, nnz, q, degree, 8, 1),
-        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"each step: Clenshaw degree steps (oracle maspmm T_i=256/T_k=64 + array update, "
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": f"each step: Clenshaw degree steps ({CPU_WHAT[kind]} T_i=256/T_k=64 + array update, "
                                    f"-O3 no -march, OpenMP) of ONE 64-column panel of the q={q} block, scaled by "
                                    f"ceil(q/64) = {panels} (maspmm's column-block loop); {tot_steps} degree steps "
                                    f"over {args.steps} timed samples; ms_per_step = one sample's wall time"},
@@ -312,7 +329,7 @@ def end_to_end_solves(adp, configs, device, with_cpu: bool):
                                                       (res.bounds.lambda_min, res.bounds.lambda_max), "f64", None))
             k_max = max(k1, int(math.ceil(2.5 * k1)))
             col_steps = k_max * 30 + sum(r.degree * r.active_width for r in res.history)
-            sec_step, steps, threads, _, _ = cpu_sample(a, 64, 4.0)
+            sec_step, steps, threads, _, _, _ = cpu_sample(a, 64, 4.0)
             d["cpu_projected_seconds"] = round(col_steps * sec_step / 64, 2)
             d["cpu_projection"] = (f"PROJECTION: oracle degree-step time (q=64, {threads} threads: "
                                    f"{1e3 * sec_step:.2f} ms) x {col_steps} column-steps of the GPU run's filter work")
@@ -524,9 +541,9 @@ def run_ours(args):
 
     cpu = None
     if not args.no_cpu_baseline:
-        sec_step, steps, threads, panels, sec = cpu_sample(a, q, args.cpu_seconds)
-        cpu = {"value": round(b_step / sec_step / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{steps} Clenshaw degree steps of one 64-column panel of the same operator (oracle maspmm "
+        sec_step, steps, threads, panels, sec, kind = cpu_sample(a, q, args.cpu_seconds)
+        cpu = {"value": round(b_step / sec_step / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+               "sample": f"{steps} Clenshaw degree steps of one 64-column panel of the same operator ({CPU_WHAT[kind]} "
                          f"T_i=256/T_k=64 + array update, OpenMP, -O3 no -march), {sec:.1f} s, scaled by "
                          f"ceil(q/64) = {panels}"}
 

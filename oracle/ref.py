@@ -127,3 +127,28 @@ def adaptive_degree(coeffs, k_max, l1, l2, ritz, e_i, tau_a):
     _ok(lib().ref_adaptive_degree(_p(c), C.c_int(k_max), C.c_double(l1), C.c_double(l2), _p(r), C.c_int64(len(r)),
                                   C.c_int64(e_i), C.c_double(tau_a), C.byref(out)), "adaptive_degree")
     return out.value
+
+
+class Tiled:
+    """The reference's TiledMatrix (csr_to_tiled, tiled_matrix.hpp:58-94) kept alive for timing."""
+
+    def __init__(self, a, t_i=256, t_k=64):
+        rp, ci, v = _csr(a)
+        lib().ref_tiled_create.restype = C.c_void_p
+        self.h = lib().ref_tiled_create(C.c_int64(a.n_rows), _p(rp), _p(ci), _p(v), C.c_int64(t_i), C.c_int64(t_k))
+        if not self.h:
+            raise RuntimeError("csr_to_tiled: reference raised")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_tiled_destroy(C.c_void_p(self.h))
+            self.h = None
+
+
+def bench_clenshaw_steps(t: Tiled, q, steps):
+    """(seconds, checksum) of `steps` middle Clenshaw steps: the reference's maspmm on its own tiling + the
+    one-pass array update (ref_capi.cpp), on all OpenMP threads."""
+    sec, cs = C.c_double(), C.c_double()
+    _ok(lib().ref_bench_clenshaw_steps(C.c_void_p(t.h), C.c_int64(q), C.c_int(steps), C.byref(sec), C.byref(cs)),
+        "bench_clenshaw_steps")
+    return sec.value, cs.value

@@ -3,6 +3,7 @@
 // not in this image: the stand-in covers the elementwise subset this path uses, see its header).
 // Output: oracle/_ref/libadapoly_ref.so (git-ignored). Test infrastructure: tests/test_ref_build.py checks
 // the oracle restatement (oracle/oracle.cpp) bit for bit against it.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -144,6 +145,52 @@ int ref_eval_filter(const double* coeffs, int k_max, double l1, double l2, const
     if (clamped) *clamped = c;
   });
 }
+// CPU baseline timing: `steps` middle Clenshaw steps (cheb_filter.cpp:167-173) on block-layout operands.
+// csr_to_tiled, BlockMatrix, set_zero and maspmm are the reference's own code (tiled_matrix.hpp: plain
+// C++ + OpenMP, no Eigen inside); the array update is written as the single pass Eigen's expression
+// template generates for `v = 2 l1 aw + 2 l2 w - v + c y` (one thread, one loop over the block) -- the
+// stand-in's eager temporaries would make it several passes and the reference look slower than it is.
+void* ref_tiled_create(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, int64_t t_i, int64_t t_k) {
+  try {
+    return new TiledMatrixd(csr_to_tiled(make_csr(n, n, rp, ci, v), t_i, t_k));
+  } catch (const std::exception&) {
+    return nullptr;
+  }
+}
+void ref_tiled_destroy(void* h) { delete static_cast<TiledMatrixd*>(h); }
+int ref_bench_clenshaw_steps(const void* h, int64_t q, int steps, double* seconds, double* checksum) {
+  return guarded([&] {
+    const TiledMatrixd& t = *static_cast<const TiledMatrixd*>(h);
+    const index_t n = t.n_rows;
+    const index_t t_k = t.t_k;
+    BlockMatrixd y(n, q, t_k), w(n, q, t_k), vv(n, q, t_k), aw(n, q, t_k);
+    const Philox4x32 rng(7, 7);
+    const index_t sz = y.size();
+#pragma omp parallel for schedule(static)
+    for (index_t i = 0; i < sz; ++i) {
+      y.data()[i] = rng.uniform(static_cast<std::uint64_t>(i)) - 0.5;
+      w.data()[i] = 0.5 * y.data()[i];
+      vv.data()[i] = 0.25 * y.data()[i];
+    }
+    const double two_l1 = 0.25, two_l2 = -0.5, cj = 0.01;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int s = 0; s < steps; ++s) {
+      aw.set_zero();
+      maspmm(t, w, aw);
+      double* vd = vv.data();
+      const double* ad = aw.data();
+      const double* wd = w.data();
+      const double* yd = y.data();
+      for (index_t i = 0; i < sz; ++i) vd[i] = two_l1 * ad[i] + two_l2 * wd[i] - vd[i] + cj * yd[i];
+      std::swap(vv, w);
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double cs = 0.0;
+    for (index_t i = 0; i < sz; i += 97) cs += w.data()[i];
+    *checksum = cs;
+  });
+}
+
 int ref_initial_degree(double alpha, double beta, double c, int* out) {
   return guarded([&] { *out = initial_degree(alpha, beta, c); });
 }
