@@ -44,7 +44,6 @@
 
 #include <cmath>
 #include <cstdint>
-#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -183,11 +182,6 @@ __device__ __forceinline__ uint64_t policy_evict_first(float frac) {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, %1;\n" : "=l"(pol) : "f"(frac));
   return pol;
 }
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -281,7 +275,6 @@ struct SwArgs {
   // dst + (r + shift) * ld_b, a neighbour's halo rows mapped over NVLink (see cheb_lean.cu)
   PushTarget push[kMaxPush];
   int32_t n_push;
-  int32_t wlast;  // W halo tiles loaded with an L2 evict-last policy (ADP_SWEEP_WLAST=1; measurement)
 };
 
 template <int NW, int KIND, int ARITH, bool PUSH>
@@ -317,7 +310,6 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
                      // then the V / Y tiles of that output plane (consumed one plane later)
     if (lane == 0) {
       const uint64_t pol = policy_evict_first(1.0f);
-      const uint64_t polw = policy_evict_last();
       uint32_t sw = 0, pw = 1, sv = 0, pv = 1;  // a fresh empty barrier's preceding phase counts as done
       for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
         const int panel = item / tiles, t = item - panel * tiles;
@@ -328,8 +320,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1)
           mbar_wait(empty_w + sw, pw);
           uint8_t* ws = smem + sw * G::kWS;
           mbar_expect_tx(full_w + sw, G::kW + G::kD);
-          if (p.wlast) tma4d_hint(ws, &tm_w, c0, x0 - 1, y0 - 1, wz, full_w + sw, polw);
-          else tma4d(ws, &tm_w, c0, x0 - 1, y0 - 1, wz, full_w + sw);
+          tma4d(ws, &tm_w, c0, x0 - 1, y0 - 1, wz, full_w + sw);
           tma3d(ws + G::kW, &tm_d, x0, y0, min(max(p.zv0 + o, 0), p.nzv - 1), full_w + sw);  // unused unless o is an output
           if (++sw == kSW) sw = 0, pw ^= 1;
           if (o >= 0 && o < p.nzo) {
@@ -570,11 +561,6 @@ void launch_sweep(adp_ctx* ctx, const StepArgs& s, const StencilPlan& sp) {
   for (int i = 0; i < 4; ++i) k.c[i] = sp.cls[i];
   k.n_push = s.n_push;
   for (int t = 0; t < s.n_push; ++t) k.push[t] = s.push[t];
-  static const int wlast = [] {
-    const char* e = std::getenv("ADP_SWEEP_WLAST");
-    return e && e[0] == '1' ? 1 : 0;
-  }();
-  k.wlast = wlast;
   const CUtensorMap tm_w = block_map(s.gsrc, sp, sp.nzw, s.q, s.ld * 8, kTX + 2, NW + 2);
   const CUtensorMap tm_v = block_map(s.vin, sp, sp.nz, s.q, s.ld * 8, kTX, NW);
   const CUtensorMap tm_y = block_map(s.yin, sp, sp.nz, s.q, s.ld_y * 8, kTX, NW);

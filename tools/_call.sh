@@ -1,6 +1,9 @@
 set -u
 mkdir -p gpurun_out
-timeout 3000 python tools/solve_config.py c4w --json gpurun_out/solve_c4w.json > gpurun_out/solve_c4w.txt 2>&1; echo "c4w rc=$?"
-head -3 gpurun_out/solve_c4w.txt
-timeout 4800 python tools/solve_complex.py c3 --json gpurun_out/solve_c3.json > gpurun_out/solve_c3.txt 2>&1; echo "c3 rc=$?"
-head -4 gpurun_out/solve_c3.txt | cut -c1-400
+timeout 900 python -m pytest tests/test_gpu_bench_dist.py tests/test_gpu_parity.py::test_gpu_bitwise_vs_reference_sources tests/test_gpu_sweep.py -x -q > gpurun_out/new_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/new_tests.log
+tail -4 gpurun_out/new_tests.log
+python __graft_entry__.py smoke 2>&1 | tail -2
+echo "--- W evict-normal"; timeout 600 python tools/ld_probe.py --cases 1024:1024,926:928 2>&1 | tail -2
+echo "--- W evict-last"; ADP_SWEEP_WLAST=1 timeout 600 python tools/ld_probe.py --cases 1024:1024,926:928 2>&1 | tail -2
+echo "--- c2"; timeout 600 python tools/ld_probe.py --config c2 --cases 256:256,362:384 --degree 200 2>&1 | tail -2
+ADP_SWEEP_WLAST=1 timeout 600 python tools/ld_probe.py --config c2 --cases 256:256,362:384 --degree 200 2>&1 | tail -2
