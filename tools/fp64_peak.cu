@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 constexpr int kChains = 8;
 
@@ -58,7 +59,33 @@ double run(int sms, double* out, int iters) {
   return ops / (best * 1e-3);  // instructions (per lane) per second
 }
 
-int main() {
+// Sustained mode (`fp64_peak <seconds>`): DFMA launches back to back for that long, one event pair around
+// the whole run -- the throughput the pipe holds under the board's power cap (tools/fp64_power.py samples
+// power and SM clock beside it).
+double sustained(int sms, double* out, double seconds) {
+  const int grid = sms * 8, block = 256, iters = 200000;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fp64_loop<0><<<grid, block>>>(out, iters, 0.999999, 1e-9);
+  cudaDeviceSynchronize();
+  cudaEventRecord(e0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  int launches = 0;
+  float ms = 0.f;
+  cudaEventRecord(e0);
+  while (ms < seconds * 1e3) {
+    for (int k = 0; k < 4; ++k, ++launches) fp64_loop<0><<<grid, block>>>(out, iters, 0.999999, 1e-9);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  const double ops = static_cast<double>(grid) * block * iters * kChains * launches;
+  return ops / (ms * 1e-3);
+}
+
+int main(int argc, char** argv) {
   int dev = 0, sms = 0, clk_khz = 0;
   cudaSetDevice(dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -67,6 +94,13 @@ int main() {
   if (cudaMalloc(&out, sizeof(double) * sms * 8 * 256) != cudaSuccess) {
     std::printf("{\"error\": \"cudaMalloc failed\"}\n");
     return 1;
+  }
+  if (argc > 1) {
+    const double secs = std::atof(argv[1]);
+    const double fma_s = sustained(sms, out, secs > 0.5 ? secs : 0.5);
+    std::printf("{\"dfma_sustained_tflops\": %.3f, \"seconds\": %.1f}\n", 2.0 * fma_s / 1e12, secs);
+    cudaFree(out);
+    return 0;
   }
   const int iters = 20000;
   const double fma = run<0>(sms, out, iters);
