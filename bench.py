@@ -415,10 +415,12 @@ def secondary(adp, configs, device, peak, fpk):
             serial_ms = flops / (fpk[0] * 1e9) + dram / (peak * 1e6)
             d["serial_bound_ms"] = round(serial_ms, 1)
             d["frac_of_serial_bound"] = round(serial_ms / launch_ms, 4)
+            d["overlap_bound_ms"] = round(max(flops / (fpk[0] * 1e9), dram / (peak * 1e6)), 1)
             d["note"] = ("complex MAC = 4 DFMA (8 flops). Two resources bound this step: the FP64 pipe (flops / measured "
-                         "DFMA peak) and DRAM (streams + ~40 random off-band W row panels per row, 1.1 TB). Each peak "
-                         "was measured alone at ~1 kW; under the 1 kW cap they cannot both run at peak, so the step "
-                         "is compared with their sum (serial_bound_ms) as well as with each alone")
+                         "DFMA peak) and DRAM (streams + ~40 random off-band W row panels per row, 1.1 TB). Alone, a "
+                         "copy at the DRAM peak draws the whole 1 kW cap and DFMA at its peak 590 W "
+                         "(profiles/fp64_peak.json), so under the cap they overlap only partly: the step lies between "
+                         "overlap_bound_ms (max of the two) and serial_bound_ms (their sum)")
         out[name] = d
         del x, y
         da.close()
