@@ -1,2 +1,14 @@
 set -u
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,l1tex__t_sector_hit_rate.pct,lts__t_sector_hit_rate.pct,sm__warps_active.avg.per_cycle_active,l1tex__throughput.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:cheb_lean_kernel -s 7 -c 3 python tools/tune_step.py --config c3 --variants 2 --degree 6 --reps 1 2>&1 | grep -E "cheb_lean_kernel|l1tex|gpu__time|lts__|dram__|warps_active|issue_active" | cut -c1-170
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/gpu_tests.log
+tail -3 gpurun_out/gpu_tests.log
+python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log > gpurun_out/bench_ref.json; cut -c1-200 gpurun_out/bench_ref.json
+timeout 1500 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?"
+grep '"metric"' gpurun_out/bench_full.log | tail -1 > gpurun_out/bench_full.json
+python - <<'P'
+import json
+d=json.load(open('gpurun_out/bench_full.json'))
+print(d['value'], d['roofline']['frac'], d['roofline']['launch_ms'], d['e2e']['value'], d['clocks'], d['cpu_baseline']['value'])
+for k,v in d['configs'].items(): print(k, v['step_launch_ms'], v.get('frac_of_hbm_peak'), v.get('frac_of_fp64_peak'), v.get('frac_of_serial_bound'), v.get('overlap_bound_ms'))
+P
