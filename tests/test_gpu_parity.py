@@ -262,6 +262,17 @@ def test_config1_full_size_bitwise(ctx, orc):
     oa = orc.Csr(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)
     got = adp.clenshaw_apply(f, adp.DeviceCsr(a, ctx), x, k)
     assert_bitwise(got, orc.clenshaw_apply(g, orc.Tiled(oa, 256, 64), x, k))
+    # BASELINE.json configs[0] at its full size and block width against the REFERENCE's own clenshaw_apply
+    # (oracle/_ref: its sources compiled against the Eigen stand-in), on the reference's own Philox block
+    from oracle import ref
+
+    if ref.available():
+        coeffs, l1, l2, _, _ = ref.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, int(np.ceil(2.5 * k)), 0.5)
+        assert np.array_equal(coeffs, f.coeff_array())
+        xr = ref.fill_gaussian(a.n_rows, cfg.q, 0, 0)
+        assert np.array_equal(xr, x)
+        want, _ = ref.clenshaw_apply(coeffs, len(coeffs) - 1, l1, l2, oa, 256, 64, xr, k)
+        assert_bitwise(got, want)
 
 
 @pytest.mark.slow

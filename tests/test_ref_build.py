@@ -119,3 +119,20 @@ def test_scalar_filter_and_degrees_bitwise():
         for tau in (1e-1, 1e-3, 1e-8):
             assert orc.adaptive_degree(f, ritz, e_i, tau) == ref.adaptive_degree(f.coeffs, f.k_max, f.l1, f.l2, ritz,
                                                                                  e_i, tau)
+
+
+def test_config1_full_size_bitwise():
+    # BASELINE.json configs[0] (the reference's own CPU-runnable case) at full size: 40^3 7-point Laplacian +
+    # potential, block 64, the configuration's initial degree -- oracle restatement vs the reference's sources
+    from paper_2604_00914_b200 import configs
+
+    configs.set_rng(orc.uniform_range, orc.gaussian_range)  # the oracle's Philox: no product library needed
+    cfg = configs.CONFIGS["c1"]
+    a = cfg.operator()
+    oa = orc.Csr(a.n_rows, a.n_cols, a.row_ptr, a.col_idx, a.values)
+    k = configs.filter_degree(cfg)
+    f = orc.build_filter(cfg.window[0], cfg.window[1], cfg.bounds, int(np.ceil(2.5 * k)), 0.5)
+    x = orc.fill_gaussian(a.n_rows, cfg.q, 0, 0)
+    got = orc.clenshaw_apply(f, orc.Tiled(oa, 256, 64), x, k)
+    want, _ = ref.clenshaw_apply(f.coeffs, f.k_max, f.l1, f.l2, oa, 256, 64, x, k)
+    assert np.array_equal(got, want)
