@@ -10,9 +10,16 @@
 // traffic, and R independent accumulator sets per lane for the FP64 pipe.
 //
 // Per row the products still accumulate in ascending column order -- its lower off-band entries
-// (row by row, before the sweep), its band (during the sweep, column ascending), its upper off-band
-// entries (after it) -- which is CSR order, so the result is bitwise the lean kernel's (complex: four
+// (before the sweep), its band (during the sweep, column ascending), its upper off-band entries
+// (after it) -- which is CSR order, so the result is bitwise the lean kernel's (complex: four
 // DFMA per entry, the order the complex path defines; real: the reference's unfused mul + add).
+//
+// What makes it run (each step measured on config 5 at full size): the band's operator
+// values are loaded coalesced one chunk AHEAD and read back from the warp's shared-memory slot as
+// broadcasts with compile-time offsets (values loaded at use: 1051 ms; staged: 485-522 ms); the
+// off-band W row panels -- random rows, each a DRAM round trip -- land through a ring of cp.async stages
+// in the same slot, L1 bypassed; and ONE gather code path serves both off-band phases, because at 52K
+// instructions the kernel fell out of the instruction cache (743 ms; compact: 391-417 ms, power-bound).
 //
 // The host derives h from the middle row and a device kernel verifies, for EVERY row, that its
 // columns are [lower off-band | max(0, r - h) .. min(n - 1, r + h) | upper off-band] and records
