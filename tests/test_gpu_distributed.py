@@ -54,8 +54,15 @@ def make_backend(mailbox, rank):
             return [(buf, (peer, rank, self.calls)) for kind, peer, buf in ops if kind == "recv"]
 
         def exchange_wait(self, pending):
+            # the posted clone lives in the SENDER's stream pool of the caching allocator: finish the copy
+            # before dropping the last reference, or the sender may reuse the memory while this rank's
+            # stream still reads it (seen as corrupted halo planes on 64^3 grids; NCCL's own exchange
+            # records the streams itself)
             for buf, key in pending:
-                buf.copy_(mailbox.take(key))
+                src = mailbox.take(key)
+                buf.copy_(src)
+                torch.cuda.current_stream().synchronize()
+                del src
 
     return ThreadBackend()
 
@@ -83,27 +90,56 @@ def run_ranks(a, world, fn):
     return results
 
 
-@pytest.mark.parametrize("world,degree,q", [(2, 12, 64), (3, 7, 6), (2, 1, 130), (4, 20, 256)])
-def test_emulated_ranks_bitwise(orc, world, degree, q):
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world,degree,q,kind", [(2, 12, 64, "lap"), (3, 7, 6, "lap"), (2, 1, 130, "lap"),
+                                                  (4, 20, 256, "lap"),
+                                                  # slabs of whole grid planes (bench.py --gpus N --halo nccl, and
+                                                  # solve_sharded without peer memory): the plane-sweep kernel on the
+                                                  # interior slab and on the one-plane boundary launches
+                                                  (2, 12, 64, "lap_planes"), (4, 9, 100, "lap_planes"),
+                                                  (2, 8, 64, "27pt_planes"), (3, 11, 40, "27pt_planes"),
+                                                  # more (panel, tile) items than SMs: every persistent CTA of the
+                                                  # sweep kernel walks several items of a RANGED launch
+                                                  (2, 5, 64, "27pt40_planes"), (2, 5, 256, "27pt40_planes"),
+                                                  (3, 4, 117, "27pt40_planes"), (2, 6, 256, "lap40_planes"),
+                                                  (2, 5, 117, "27pt64_planes"), (2, 3, 128, "27pt64_planes")])
+def test_emulated_ranks_bitwise(orc, world, degree, q, kind):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    import bench
     from paper_2604_00914_b200 import configs
     from paper_2604_00914_b200.distributed import DistributedFilter
 
-    a = configs.laplacian7_potential(20, -2.0, 2.0, seed=1)
+    import re
+
+    m = re.search(r"(\d+)_planes", kind)
+    if kind.startswith("lap"):
+        nx = int(m.group(1)) if m else 20
+        a, plane = configs.laplacian7_potential(nx, -2.0, 2.0, seed=1), nx * nx
+        f = adp.build_filter(5.9, 6.1, (-2.0, 14.0), 40, 0.5)
+    else:
+        nx = int(m.group(1)) if m else 12
+        a, plane = configs.dft_like_27pt(nx, 4, 2), nx * nx
+        f = adp.build_filter(0.2, 0.6, (-5.9, 8.6), 40, 0.5)
+    ranges = bench.plane_ranges(a.n_rows, plane, world) if kind.endswith("_planes") else None
     n = a.n_rows
-    f = adp.build_filter(5.9, 6.1, (-2.0, 14.0), 40, 0.5)
     x = orc.fill_gaussian(n, q, 3, 0)
     want = adp.clenshaw_apply(f, adp.DeviceCsr(a), x, degree)
+    kernels = [None] * world
 
     def fn(rank, be):
-        df = DistributedFilter(a, be, rank, world)
+        df = DistributedFilter(a, be, rank, world, ranges)
         r0, r1 = df.ranges[rank]
-        xl = torch.from_numpy(np.ascontiguousarray(x[r0:r1])).cuda()
-        return df.apply(f.coeffs, f.l1, f.l2, xl, degree).cpu().numpy()
+        xl = be.alloc(r1 - r0, q)  # the backend's block pitch (odd widths need the pad column)
+        xl.copy_(torch.from_numpy(np.ascontiguousarray(x[r0:r1])))
+        out = df.apply(f.coeffs, f.l1, f.l2, xl, degree).cpu().numpy()
+        kernels[rank] = be.ctx.last_step_kernel
+        return out
 
     got = np.concatenate(run_ranks(a, world, fn))
     assert np.array_equal(got, want)
+    if ranges is not None and degree >= 2:
+        assert all(k == 5 for k in kernels), kernels  # every rank's Step launches took the plane-sweep kernel
 
 
 # ------------------------------------------------ halo pushed by the step kernel (peer memory) ---
