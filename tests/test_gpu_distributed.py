@@ -157,7 +157,11 @@ def test_emulated_ranks_bitwise(orc, world, degree, q, kind):
                                                   # slabs of whole grid planes: the plane-sweep kernel on the
                                                   # interior AND on the pushed boundary planes
                                                   (2, 12, 64, "lap_planes"), (3, 9, 40, "27pt_planes"),
-                                                  (4, 6, 34, "27pt_planes")])
+                                                  (4, 6, 34, "27pt_planes"),
+                                                  # more (panel, tile) items than SMs on the interior slabs AND on
+                                                  # the one-plane push launches (the multi-GPU bench's shape:
+                                                  # config 4 has 8192 items per launch)
+                                                  (2, 5, 256, "27pt40_planes"), (3, 4, 200, "lap40_planes")])
 def test_peer_halo_lockstep_bitwise(orc, world, degree, q, kind):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -168,11 +172,13 @@ def test_peer_halo_lockstep_bitwise(orc, world, degree, q, kind):
     if kind == "herm":  # config 3's structure: complex128 blocks through alloc, steps and pushes
         a = configs.peierls_lattice(24)
     else:
-        a = configs.laplacian7_potential(20, -2.0, 2.0, seed=1) if kind.startswith("lap") else configs.dft_like_27pt(12, 4, 2)
+        big = "40" in kind
+        a = (configs.laplacian7_potential(40 if big else 20, -2.0, 2.0, seed=1) if kind.startswith("lap")
+             else configs.dft_like_27pt(40 if big else 12, 4, 2))
     if kind.endswith("_planes"):
         import bench
 
-        plane = 400 if kind.startswith("lap") else 144
+        plane = (1600 if big else 400) if kind.startswith("lap") else (1600 if big else 144)
         ranges = bench.plane_ranges(a.n_rows, plane, world)
     n = a.n_rows
     f = adp.build_filter(5.9, 6.1, (-2.0, 14.0), 40, 0.5) if kind != "herm" else adp.build_filter(-0.3, 0.2, (-5.0, 5.0), 40, 0.5)
