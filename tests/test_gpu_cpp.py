@@ -24,3 +24,23 @@ def test_cpp_caller_on_gpu():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr + r.stdout
     assert "bitwise==oracle" in r.stdout
+
+
+SHIM = os.path.join(ROOT, "tests", "cpp", "ref_shim_test")
+
+
+@pytest.mark.gpu
+def test_reference_side_shim_on_gpu():
+    # tests/cpp/adapoly_gpu_shim.hpp is INTEGRATION.md's binding; ref_shim_test compiles it against the
+    # REFERENCE's own headers and cheb_filter.cpp (in place under /root/reference, Eigen stand-in) and
+    # compares gpu::clenshaw_apply / gpu::maspmm with the reference's CPU functions bitwise, the spmv
+    # accounting and the exception types. Built where the reference tree exists; travels prebuilt.
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    if not os.path.exists(SHIM):
+        pytest.skip("ref_shim_test not built (no /root/reference where the repo was built)")
+    r = subprocess.run([SHIM], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr + r.stdout
+    assert "bitwise==reference" in r.stdout and "exceptions mapped" in r.stdout
