@@ -46,11 +46,12 @@ def make_backend(mailbox, rank):
 
         def exchange_start(self, ops):
             self.calls += 1
+            # clone on this rank's stream and FINISH before posting: the receiver copies on its own stream
+            # and must not overtake the clone (seen at 128^3: 60 MB halo planes)
+            clones = [(peer, buf.clone()) for kind, peer, buf in ops if kind == "send"]
             torch.cuda.current_stream().synchronize()
-            for kind, peer, buf in ops:
-                if kind == "send":
-                    mailbox.post((rank, peer, self.calls), buf.clone())
-            torch.cuda.synchronize()
+            for peer, c in clones:
+                mailbox.post((rank, peer, self.calls), c)
             return [(buf, (peer, rank, self.calls)) for kind, peer, buf in ops if kind == "recv"]
 
         def exchange_wait(self, pending):

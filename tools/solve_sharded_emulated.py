@@ -120,7 +120,7 @@ def main():
            "sharded": {"eigenpairs": len(ev), "iterations": results[0].iterations, "p": results[0].subspace_dim,
                        "seconds_emulated": round(t_sh, 1), "converged": bool(all(r.converged for r in results)),
                        "ranks_agree_bitwise": bool(ranks_agree), "last_step_kernel_per_rank": kernels,
-                       "max_residual_on_A": float(res.max()), "tolerance": 1e-10 * scale,
+                       "max_residual_on_A": float(res.max()) if res.numel() else None, "tolerance": 1e-10 * scale,
                        "orthonormality_fro": orth},
            "same_count": bool(same_count), "eigenvalues_max_rel_diff_vs_single": rel,
            "note": "ranks are threads on one GPU (no rank's kernel waits on another's): a correctness record of the "
