@@ -38,20 +38,23 @@ def main():
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--window", default="0.300,0.306")
     ap.add_argument("--json", default="")
+    ap.add_argument("--lattice", type=int, default=0, help="complex Peierls lattice L x L (config 3's structure) "
+                    "in balanced row ranges instead of the 27-point operator; single reference: solve_hermitian")
     args = ap.parse_args()
     from paper_2604_00914_b200.distributed import DistributedFilter
     from paper_2604_00914_b200.sharded import ShardedSolver, ShardSparse, TorchOps
 
     lo, hi = (float(v) for v in args.window.split(","))
-    a = configs.dft_like_27pt(args.nx)
+    cplx = args.lattice > 0
+    a = configs.peierls_lattice(args.lattice) if cplx else configs.dft_like_27pt(args.nx)
     n, world = a.n_rows, args.world
     cfg = adp.SolverConfig(interval_a=lo, interval_b=hi, rng_seed=0)
     ctx = adp.Context(0)
     t0 = time.perf_counter()
-    one = adp.solve(adp.DeviceCsr(a, ctx), cfg)
+    one = adp.solve_hermitian(adp.DeviceCsr(a, ctx), cfg) if cplx else adp.solve(adp.DeviceCsr(a, ctx), cfg)
     torch.cuda.synchronize()
     t_one = time.perf_counter() - t0
-    print(f"single GPU (C++ solve): n {n} nnz {a.nnz} window {(lo, hi)} -> {len(one.eigenvalues)} eigenpairs, "
+    print(f"single GPU solve: n {n} nnz {a.nnz} window {(lo, hi)} -> {len(one.eigenvalues)} eigenpairs, "
           f"{one.iterations} iterations, p {one.subspace_dim}, {t_one:.1f} s, max residual {one.max_residual:.3e}", flush=True)
     # torch.linalg initialises its backend lazily and not thread-safely ("lazy wrapper should be called at most
     # once" when two threads race into it): touch it once before the rank threads start
@@ -60,7 +63,7 @@ def main():
     torch.linalg.eigh(eye)
     torch.linalg.solve_triangular(eye, eye, upper=True, left=False)
     torch.cuda.synchronize()
-    ranges = bench.plane_ranges(n, args.nx * args.nx, world)
+    ranges = None if cplx else bench.plane_ranges(n, args.nx * args.nx, world)
     mailbox = Mailbox()
     shared = {"cv": threading.Condition(), "gen": 0, "count": 0, "slots": {}, "result": None}
     results, errors, kernels = [None] * world, [], [None] * world
@@ -70,7 +73,7 @@ def main():
             be = make_backend(mailbox, rank)
             with torch.cuda.stream(be.stream):
                 df = DistributedFilter(a, be, rank, world, ranges)
-                s = ShardedSolver(n, False, TorchOps(False), ShardSparse(df), ThreadComm(shared, rank, world))
+                s = ShardedSolver(n, cplx, TorchOps(cplx), ShardSparse(df), ThreadComm(shared, rank, world))
                 results[rank] = s.solve(cfg)
                 torch.cuda.current_stream().synchronize()
                 kernels[rank] = be.ctx.last_step_kernel
@@ -111,10 +114,12 @@ def main():
     lam = torch.as_tensor(ev, device=vecs.device)
     res = torch.linalg.vector_norm(av - vecs * lam[None, :], dim=0)
     scale = max(abs(one.bounds.lambda_min), abs(one.bounds.lambda_max))
-    gram = vecs.T @ vecs
+    gram = vecs.conj().T @ vecs
     orth = float(torch.linalg.matrix_norm(gram - torch.eye(gram.shape[0], dtype=gram.dtype, device=gram.device)))
-    out = {"operator": f"27-point Mehrstellen {args.nx}^3 + Gaussian-sum potential (config 4's structure)", "n": n,
-           "nnz": a.nnz, "window": [lo, hi], "world": world, "row_ranges": [list(r) for r in ranges],
+    desc = (f"complex Peierls lattice {args.lattice}^2 (config 3's structure)" if cplx
+            else f"27-point Mehrstellen {args.nx}^3 + Gaussian-sum potential (config 4's structure)")
+    out = {"operator": desc, "n": n,
+           "nnz": a.nnz, "window": [lo, hi], "world": world, "row_ranges": [list(r) for r in ranges] if ranges else "balanced rows",
            "single": {"eigenpairs": len(one.eigenvalues), "iterations": one.iterations, "p": one.subspace_dim,
                       "seconds": round(t_one, 1), "max_residual": one.max_residual},
            "sharded": {"eigenpairs": len(ev), "iterations": results[0].iterations, "p": results[0].subspace_dim,
